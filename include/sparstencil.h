@@ -1,0 +1,166 @@
+/*
+ * sparstencil.h — C ABI of the B200-native SparStencil engine.
+ *
+ * Plain C types only (pointers, sizes, integers); no torch or C++ types.
+ * Every function returns an sst_status; on failure sst_last_error() returns a
+ * thread-local message. Status codes map one-to-one onto the exception types
+ * the reference C++ API throws:
+ *   SST_ERR_INVALID_ARGUMENT <-> std::invalid_argument
+ *   SST_ERR_LOGIC            <-> std::logic_error
+ *   SST_ERR_OUT_OF_RANGE     <-> std::out_of_range
+ *   SST_ERR_RUNTIME          <-> std::runtime_error
+ * and SST_ERR_CUDA / SST_ERR_NO_DEVICE for device failures (the engine never
+ * falls back to a CPU path: no device means an error).
+ *
+ * Reference interfaces replaced (proj/ = /root/reference/proj):
+ *   sst_compile            flatten + crush + convert_layout + compress_24
+ *                          (layout.hpp:80-82, convert.hpp:101, emulator.hpp:45;
+ *                          orchestrated as in pipeline.cpp:75-78, 112)
+ *   sst_compiled_s24       dump_sparse24 (emulator.hpp:68; docs/formats.md:49-63)
+ *   sst_plan_create        make_plan (codegen.hpp:65-67): the device-side KernelPlan
+ *   sst_run_steps          the hot loop: tiled_sparse_matmul + output_position
+ *                          (emulator.hpp:63-65, layout.hpp:77) repeated per time step
+ *                          with ping-pong buffers; replaces the step loop of
+ *                          direct_apply (stencil.hpp:72, stencil.cpp:239-268)
+ *   sst_apply_host         direct_apply(spec, grid, steps) end to end from host memory
+ */
+#ifndef SPARSTENCIL_H_
+#define SPARSTENCIL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SST_API __attribute__((visibility("default")))
+#else
+#define SST_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum sst_status {
+    SST_OK = 0,
+    SST_ERR_INVALID_ARGUMENT = 1,
+    SST_ERR_LOGIC = 2,
+    SST_ERR_OUT_OF_RANGE = 3,
+    SST_ERR_RUNTIME = 4,
+    SST_ERR_CUDA = 5,
+    SST_ERR_NO_DEVICE = 6
+} sst_status;
+
+/* operand precision of the tensor-core path (storage is always fp32) */
+enum { SST_PREC_F16 = 1 };
+
+/* ---------------------------------------------------------------- compile */
+
+typedef struct sst_compiled sst_compiled;
+
+/* Compile a stencil for a grid. `stencil` is a preset name (Heat-2D, ...) or a
+ * spec document (docs/formats.md:3-30). r1/r2 = 0 selects the tcgen05 layout
+ * explorer (r1*r2 = 128); fuse >= 1 applies fuse_time_steps first. */
+SST_API sst_status sst_compile(const char* stencil, const uint64_t* grid_dims, int ndims, int r1, int r2,
+                       uint64_t fuse, sst_compiled** out);
+SST_API void sst_compiled_destroy(sst_compiled* c);
+
+typedef struct sst_compile_info {
+    int32_t dims, k, r1, r2;
+    uint64_t m_prime, k_prime, n_prime;
+    uint64_t cols;          /* A'' logical columns after PIT + 4-alignment */
+    uint64_t p;             /* matching zero columns */
+    uint64_t align_cols;    /* alignment zero columns */
+    int32_t used_blossom;   /* staircase check failed -> Edmonds fallback */
+    int32_t refined;        /* n <= 24 exact refinement replaced Alg. 1 */
+    uint64_t window_w;      /* wv = kx + r1 - 1 */
+    uint64_t window_h;      /* wu = ky + r2 - 1 */
+    uint64_t window_d;      /* kz (3D) or 1 */
+    uint64_t grid_dims[3];
+} sst_compile_info;
+
+SST_API sst_status sst_compiled_info(const sst_compiled* c, sst_compile_info* info);
+/* .s24 artifact bytes; tag 0 = exact64, 1 = round16. *len receives the size;
+ * buf may be NULL to query it. */
+SST_API sst_status sst_compiled_s24(const sst_compiled* c, uint32_t tag, uint8_t* buf, size_t cap,
+                            size_t* len);
+/* permutation (original column -> position), k_prime + p entries */
+SST_API sst_status sst_compiled_perm(const sst_compiled* c, uint64_t* buf, size_t cap, size_t* len);
+/* col_origin of the converted layout, `cols` entries, UINT64_MAX = zero column */
+SST_API sst_status sst_compiled_col_origin(const sst_compiled* c, uint64_t* buf, size_t cap, size_t* len);
+/* dense A'' (m' x cols, row-major doubles) */
+SST_API sst_status sst_compiled_matrix(const sst_compiled* c, double* buf, size_t cap, size_t* len);
+
+/* ------------------------------------------------------- device plan desc */
+
+typedef struct sst_plan_desc {
+    int32_t dims;             /* 2 or 3 on the device path */
+    int32_t k;                /* kernel extent per axis (odd) */
+    int32_t r1, r2;           /* tile = r1 (x) by r2 (y) outputs, r1 * r2 == 128 */
+    uint64_t grid_dims[3];    /* slowest..fastest; unused trailing entries 0 */
+    uint64_t rows;            /* m' (== 128) */
+    uint64_t cols;            /* A'' logical columns, multiple of 4 */
+    const double* a_values;   /* rows x cols/2 compressed values (reference order) */
+    const uint8_t* a_meta;    /* rows x cols/4 bytes pos0 | pos1 << 2 */
+    const uint64_t* col_origin; /* cols entries, UINT64_MAX = zero column */
+    uint64_t window_w, window_h, window_d;
+    int32_t precision;        /* SST_PREC_F16 */
+} sst_plan_desc;
+
+/* Pointers into the compiled object; valid while `c` lives. */
+SST_API sst_status sst_compiled_plan_desc(const sst_compiled* c, sst_plan_desc* desc);
+
+/* ------------------------------------------------------------ device plan */
+
+typedef struct sst_plan sst_plan;
+
+SST_API sst_status sst_plan_create(const sst_plan_desc* desc, int device, sst_plan** out);
+SST_API void sst_plan_destroy(sst_plan* plan);
+
+/* Storage layout of one grid buffer on the device: rows padded so the first
+ * interior cell of every row is 16-byte aligned (TMA requirement). Element
+ * (z, y, x) lives at z*plane_pitch + y*row_pitch + left_pad + x. */
+typedef struct sst_storage {
+    uint64_t row_pitch;    /* elements */
+    uint64_t plane_pitch;  /* elements */
+    uint64_t left_pad;     /* elements */
+    uint64_t bytes;        /* bytes of one buffer */
+} sst_storage;
+
+SST_API sst_status sst_plan_storage(const sst_plan* plan, sst_storage* st);
+typedef struct sst_plan_stats {
+    int32_t k_pad, k_steps, tiles_x, tiles_y, patch_w, patch_h, patch_planes;
+    int32_t worst_bank_conflict;
+    int32_t smem_bytes, ctas, batches;
+    uint64_t launches;     /* kernel launches issued by this plan so far */
+} sst_plan_stats;
+SST_API sst_status sst_plan_stats_get(const sst_plan* plan, sst_plan_stats* s);
+
+/* Bind two caller-owned device buffers (each sst_storage.bytes) as the
+ * ping-pong pair. Passing NULL for both makes the plan allocate its own. */
+SST_API sst_status sst_plan_bind(sst_plan* plan, void* buf0, void* buf1);
+/* Dense grid (slowest..fastest, fp32) <-> storage buffer `which` (0/1).
+ * src/dst_on_device selects device or host memory for the dense side. */
+SST_API sst_status sst_upload(sst_plan* plan, int which, const float* src, int src_on_device,
+                      void* stream);
+SST_API sst_status sst_download(sst_plan* plan, int which, float* dst, int dst_on_device, void* stream);
+/* Run `steps` time steps starting from buffer `src`; *dst_out receives the
+ * buffer holding the result. The interior [r, N-r) of every axis is updated
+ * each step; the boundary ring keeps the input values, so after T steps the
+ * core [T*r, N-T*r) equals the reference's valid-region sweep. */
+SST_API sst_status sst_run_steps(sst_plan* plan, int src, uint64_t steps, void* stream, int* dst_out);
+/* Restrict the next sst_run_steps to output rows [y0, y1) of the slowest
+ * blocked axis (used by the multi-GPU driver to split interior / boundary
+ * work); y1 <= y0 resets to the full interior. */
+SST_API sst_status sst_set_row_window(sst_plan* plan, uint64_t y0, uint64_t y1);
+/* End to end from host memory: upload, run, download (full-size grid). */
+SST_API sst_status sst_apply_host(sst_plan* plan, const float* h_in, float* h_out, uint64_t steps);
+
+/* ----------------------------------------------------------------- misc */
+SST_API const char* sst_last_error(void);
+SST_API int sst_device_count(void);
+SST_API const char* sst_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARSTENCIL_H_ */

@@ -1,0 +1,70 @@
+"""In-tree build of libsparstencil.so (host C++20 compile library + sm_100a
+CUDA runtime/kernels behind the C ABI in include/sparstencil.h).
+
+    python -m paper_2506_22969_b200.build        # or build() from __graft_entry__
+
+Incremental by mtime; objects under paper_2506_22969_b200/build/ (git-ignored),
+the shared library next to this file so it travels to the GPU box with the
+repo snapshot. cudart is linked statically and the driver API is resolved at
+run time (cudaGetDriverEntryPoint), so the library loads on a CPU-only host.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+REPO = PKG.parent
+CSRC = PKG / "csrc"
+OBJ = PKG / "build"
+LIB = PKG / "libsparstencil.so"
+
+NVCC = os.environ.get("NVCC", "nvcc")
+CXX = os.environ.get("CXX", "g++")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+INCLUDES = [f"-I{REPO / 'include'}", f"-I{CSRC / 'host'}", f"-I{CSRC / 'device'}"]
+CXXFLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-fvisibility=hidden"]
+NVFLAGS = ["-std=c++20", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-fvisibility=hidden",
+           "--expt-relaxed-constexpr"]
+
+HOST_SRCS = sorted((CSRC / "host").glob("*.cpp"))
+DEVICE_SRCS = sorted((CSRC / "device").glob("*.cu"))
+HEADERS = sorted((CSRC).rglob("*.h*")) + sorted((REPO / "include").glob("*.h")) + sorted(
+    (CSRC / "device").glob("*.cuh"))
+
+
+def _stale(target: Path, deps) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(Path(d).stat().st_mtime > t for d in deps)
+
+
+def _run(cmd, verbose):
+    if verbose:
+        print(" ".join(str(c) for c in cmd), flush=True)
+    subprocess.run([str(c) for c in cmd], check=True)
+
+
+def build(verbose: bool = False, force: bool = False) -> Path:
+    OBJ.mkdir(exist_ok=True)
+    objs = []
+    for src in HOST_SRCS:
+        o = OBJ / (src.stem + ".o")
+        objs.append(o)
+        if force or _stale(o, [src, *HEADERS, __file__]):
+            _run([CXX, *CXXFLAGS, *INCLUDES, "-c", src, "-o", o], verbose)
+    for src in DEVICE_SRCS:
+        o = OBJ / (src.stem + ".cu.o")
+        objs.append(o)
+        if force or _stale(o, [src, *HEADERS, __file__]):
+            _run([NVCC, *NVFLAGS, *INCLUDES, "-c", src, "-o", o], verbose)
+    if force or _stale(LIB, objs):
+        _run([NVCC, "-shared", *ARCH, "-cudart", "static", "-o", LIB, *objs], verbose)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(verbose=True, force="--force" in sys.argv)

@@ -1,0 +1,424 @@
+// runtime.cu — C ABI device tier: plan creation (constant operands to HBM),
+// storage layout, TMA descriptors, the ping-pong time loop and host e2e.
+// Replaces make_plan (proj/core/src/codegen.cpp:75-102) and the verification
+// loop of run_compile (pipeline.cpp:115-153) with real device execution.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../host/capi_internal.hpp"
+#include "sparstencil.h"
+#include "stencil_kernel.cuh"
+#include "stensor/device_image.hpp"
+#include "stensor/morph.hpp"
+
+namespace {
+
+using sstc::CudaError;
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        const bool nodev = e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver;
+        throw CudaError(std::string(what) + ": " + cudaGetErrorString(e), nodev);
+    }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        ck(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q),
+           "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
+        if (!p || q != cudaDriverEntryPointSuccess)
+            throw CudaError("cuTensorMapEncodeTiled unavailable", false);
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+template <int DIMS, int TXB, int TYB>
+void configure_kernel(int smem) {
+    ck(cudaFuncSetAttribute(sst::stencil_step_kernel<DIMS, TXB, TYB>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+       "cudaFuncSetAttribute");
+}
+
+}  // namespace
+
+struct sst_plan {
+    int device = 0;
+    int dims = 2, k = 3, r = 1;
+    int gx = 0, gy = 1, gz = 1;
+    stensor::DeviceImage img;
+    int tiles_y = 8;
+    sst_storage storage{};
+    int smem = 0, num_sms = 0;
+    // device constants
+    void* d_a = nullptr;
+    uint32_t* d_e = nullptr;
+    int32_t* d_koff = nullptr;
+    uint8_t* d_korder = nullptr;
+    // ping-pong storage
+    float* buf[2] = {nullptr, nullptr};
+    bool owns_buf = false;
+    CUtensorMap tmap[2];
+    bool tmap_ok = false;
+    int64_t y_lo = 0, y_hi = -1;  // interior row window
+    uint64_t launches = 0;
+
+    ~sst_plan() {
+        cudaSetDevice(device);
+        cudaFree(d_a);
+        cudaFree(d_e);
+        cudaFree(d_koff);
+        cudaFree(d_korder);
+        if (owns_buf) {
+            cudaFree(buf[0]);
+            cudaFree(buf[1]);
+        }
+    }
+
+    int64_t interior_rows() const { return (dims == 3 ? gy : gy) - 2 * r; }
+
+    void make_tmaps() {
+        const int g = img.geo.patch_planes;
+        for (int i = 0; i < 2; ++i) {
+            cuuint64_t gdim[3] = {storage.row_pitch, static_cast<cuuint64_t>(gy),
+                                  static_cast<cuuint64_t>(gz)};
+            cuuint64_t gstride[2] = {storage.row_pitch * 4, storage.plane_pitch * 4};
+            cuuint32_t box[3] = {static_cast<cuuint32_t>(img.geo.patch_w),
+                                 static_cast<cuuint32_t>(img.geo.patch_h), static_cast<cuuint32_t>(g)};
+            cuuint32_t estride[3] = {1, 1, 1};
+            const CUresult rc = encode_fn()(&tmap[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                            static_cast<cuuint32_t>(dims), buf[i], gdim, gstride, box,
+                                            estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                            CU_TENSOR_MAP_SWIZZLE_NONE,
+                                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (rc != CUDA_SUCCESS)
+                throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(rc) + ")", false);
+        }
+        tmap_ok = true;
+    }
+
+    sst::StepParams step_params(int src) const {
+        sst::StepParams p{};
+        p.a_img = static_cast<const uint4*>(d_a);
+        p.e_words = d_e;
+        p.koff = d_koff;
+        p.korder = d_korder;
+        p.out = buf[src ^ 1];
+        p.row_pitch = static_cast<int64_t>(storage.row_pitch);
+        p.plane_pitch = static_cast<int64_t>(storage.plane_pitch);
+        p.left_pad = static_cast<int32_t>(storage.left_pad);
+        p.gx = gx;
+        p.gy = gy;
+        p.gz = gz;
+        p.r = r;
+        const int64_t rows = gy - 2 * r;
+        p.y_lo = static_cast<int32_t>(y_hi > y_lo ? y_lo : 0);
+        p.y_hi = static_cast<int32_t>(y_hi > y_lo ? std::min<int64_t>(y_hi, rows) : rows);
+        const int bw = img.geo.tiles_x * sst::kTileW, bh = tiles_y * sst::kTileH;
+        p.nbx = (gx - 2 * r + bw - 1) / bw;
+        p.nby = (p.y_hi - p.y_lo + bh - 1) / bh;
+        p.nbz = dims == 3 ? gz - 2 * r : 1;
+        p.nbatch = p.nbx * p.nby * p.nbz;
+        p.k_pad = img.geo.k_pad;
+        p.nks = img.geo.k_pad / 32;
+        p.patch_w = img.geo.patch_w;
+        p.patch_h = img.geo.patch_h;
+        p.patch_planes = img.geo.patch_planes;
+        return p;
+    }
+
+    void launch(int src, cudaStream_t st) {
+        const sst::StepParams p = step_params(src);
+        if (p.nbatch <= 0) return;
+        const int grid = std::min(p.nbatch, num_sms);
+        if (dims == 2)
+            sst::stencil_step_kernel<2, 8, 8><<<grid, sst::kThreads, smem, st>>>(tmap[src], p);
+        else
+            sst::stencil_step_kernel<3, 8, 2><<<grid, sst::kThreads, smem, st>>>(tmap[src], p);
+        ck(cudaGetLastError(), "kernel launch");
+        ++launches;
+    }
+};
+
+extern "C" {
+
+int sst_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
+    try {
+        if (!d || !out) throw std::invalid_argument("null argument");
+        *out = nullptr;
+        if (d->precision != SST_PREC_F16) throw std::invalid_argument("unsupported precision");
+        if (d->dims != 2 && d->dims != 3)
+            throw std::invalid_argument("device path supports 2D and 3D stencils (m' = 128 needs r2 > 1)");
+        if (d->r1 != sst::kTileW || d->r2 != sst::kTileH || d->rows != 128)
+            throw std::invalid_argument("device path needs the (r1, r2) = (16, 8) layout");
+        if (d->k < 1 || d->k % 2 == 0) throw std::invalid_argument("k must be odd and >= 1");
+        int ndev = 0;
+        ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+        if (device < 0 || device >= ndev) throw CudaError("no such CUDA device", true);
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        auto P = std::make_unique<sst_plan>();
+        P->device = device;
+        P->dims = d->dims;
+        P->k = d->k;
+        P->r = (d->k - 1) / 2;
+        P->gx = static_cast<int>(d->grid_dims[d->dims - 1]);
+        P->gy = static_cast<int>(d->grid_dims[d->dims - 2]);
+        P->gz = d->dims == 3 ? static_cast<int>(d->grid_dims[0]) : 1;
+        if (P->gx < d->k || P->gy < d->k || P->gz < (d->dims == 3 ? d->k : 1))
+            throw std::invalid_argument("grid smaller than kernel");
+
+        stensor::BatchGeometry geo;
+        geo.dims = d->dims;
+        geo.k = d->k;
+        geo.tiles_x = 8;
+        geo.tiles_y = d->dims == 2 ? 8 : 2;
+        P->tiles_y = geo.tiles_y;
+        geo.patch_planes = d->dims == 3 ? d->k : 1;
+        geo.patch_h = static_cast<int>(d->window_h) + sst::kTileH * (geo.tiles_y - 1);
+        // storage: interior column r lands on a 16-byte boundary
+        const uint64_t lp = (4 - static_cast<uint64_t>(P->r) % 4) % 4;
+        // the patch is loaded from the 16-byte aligned storage column X0, i.e.
+        // lp cells left of the window origin (TMA box starts must be aligned)
+        geo.x_shift = static_cast<int>(lp);
+        geo.patch_w = static_cast<int>(sst::align_up(
+            static_cast<uint32_t>(lp + d->window_w + sst::kTileW * (geo.tiles_x - 1)), 4));
+        std::vector<std::size_t> origin(d->cols);
+        for (std::size_t i = 0; i < d->cols; ++i)
+            origin[i] = d->col_origin[i] == UINT64_MAX ? stensor::npos
+                                                       : static_cast<std::size_t>(d->col_origin[i]);
+        P->img = stensor::build_device_image(geo, d->rows, d->cols, d->a_values, d->a_meta,
+                                             origin.data(), d->window_w, d->window_h);
+        const auto& G = P->img.geo;
+        const int nks = G.k_pad / 32;
+        const sst::SmemLayout L =
+            d->dims == 2 ? sst::smem_layout<8, 8>(nks, G.k_pad, G.patch_w, G.patch_h, G.patch_planes)
+                         : sst::smem_layout<8, 2>(nks, G.k_pad, G.patch_w, G.patch_h, G.patch_planes);
+        P->smem = static_cast<int>(L.total) + 1024;  // slack for the 1 KiB base alignment
+        int max_smem = 0;
+        ck(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device),
+           "cudaDeviceGetAttribute");
+        if (P->smem > max_smem)
+            throw std::invalid_argument("stencil too wide for one CTA's shared memory (" +
+                                        std::to_string(P->smem) + " B)");
+        ck(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, device),
+           "cudaDeviceGetAttribute");
+        if (d->dims == 2)
+            configure_kernel<2, 8, 8>(P->smem);
+        else
+            configure_kernel<3, 8, 2>(P->smem);
+
+        P->storage.left_pad = lp;
+        P->storage.row_pitch = (lp + static_cast<uint64_t>(P->gx) + 3) / 4 * 4;
+        P->storage.plane_pitch = P->storage.row_pitch * static_cast<uint64_t>(P->gy);
+        P->storage.bytes = P->storage.plane_pitch * static_cast<uint64_t>(P->gz) * 4;
+
+        ck(cudaMalloc(&P->d_a, P->img.a_smem.size() * 2), "cudaMalloc");
+        ck(cudaMemcpy(P->d_a, P->img.a_smem.data(), P->img.a_smem.size() * 2, cudaMemcpyHostToDevice),
+           "cudaMemcpy");
+        ck(cudaMalloc(&P->d_e, P->img.e_words.size() * 4), "cudaMalloc");
+        ck(cudaMemcpy(P->d_e, P->img.e_words.data(), P->img.e_words.size() * 4, cudaMemcpyHostToDevice),
+           "cudaMemcpy");
+        ck(cudaMalloc(&P->d_koff, P->img.koff.size() * 4), "cudaMalloc");
+        ck(cudaMemcpy(P->d_koff, P->img.koff.data(), P->img.koff.size() * 4, cudaMemcpyHostToDevice),
+           "cudaMemcpy");
+        ck(cudaMalloc(&P->d_korder, P->img.kgroup_order.size()), "cudaMalloc");
+        ck(cudaMemcpy(P->d_korder, P->img.kgroup_order.data(), P->img.kgroup_order.size(),
+                      cudaMemcpyHostToDevice),
+           "cudaMemcpy");
+        *out = P.release();
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+void sst_plan_destroy(sst_plan* plan) { delete plan; }
+
+sst_status sst_plan_storage(const sst_plan* plan, sst_storage* st) {
+    try {
+        if (!plan || !st) throw std::invalid_argument("null argument");
+        *st = plan->storage;
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_plan_stats_get(const sst_plan* plan, sst_plan_stats* s) {
+    try {
+        if (!plan || !s) throw std::invalid_argument("null argument");
+        const auto& G = plan->img.geo;
+        *s = sst_plan_stats{};
+        s->k_pad = G.k_pad;
+        s->k_steps = G.k_pad / 32;
+        s->tiles_x = G.tiles_x;
+        s->tiles_y = plan->tiles_y;
+        s->patch_w = G.patch_w;
+        s->patch_h = G.patch_h;
+        s->patch_planes = G.patch_planes;
+        s->worst_bank_conflict = plan->img.worst_bank_conflict;
+        s->smem_bytes = plan->smem;
+        const sst::StepParams p = plan->step_params(0);
+        s->batches = p.nbatch;
+        s->ctas = std::min(p.nbatch, plan->num_sms);
+        s->launches = plan->launches;
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_plan_bind(sst_plan* plan, void* b0, void* b1) {
+    try {
+        if (!plan) throw std::invalid_argument("null plan");
+        ck(cudaSetDevice(plan->device), "cudaSetDevice");
+        if (plan->owns_buf) {
+            cudaFree(plan->buf[0]);
+            cudaFree(plan->buf[1]);
+            plan->owns_buf = false;
+        }
+        if (!b0 && !b1) {
+            ck(cudaMalloc(&plan->buf[0], plan->storage.bytes), "cudaMalloc(grid)");
+            ck(cudaMalloc(&plan->buf[1], plan->storage.bytes), "cudaMalloc(grid)");
+            plan->owns_buf = true;
+        } else {
+            if (!b0 || !b1) throw std::invalid_argument("bind needs two buffers (or none)");
+            if ((reinterpret_cast<uintptr_t>(b0) | reinterpret_cast<uintptr_t>(b1)) & 15u)
+                throw std::invalid_argument("grid buffers must be 16-byte aligned");
+            plan->buf[0] = static_cast<float*>(b0);
+            plan->buf[1] = static_cast<float*>(b1);
+        }
+        ck(cudaMemset(plan->buf[0], 0, plan->storage.bytes), "cudaMemset");
+        ck(cudaMemset(plan->buf[1], 0, plan->storage.bytes), "cudaMemset");
+        plan->make_tmaps();
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+static void copy_dense(sst_plan* plan, int which, const float* src, float* dst, bool to_storage,
+                       bool other_on_device, cudaStream_t st) {
+    if (which < 0 || which > 1) throw std::invalid_argument("buffer index must be 0 or 1");
+    if (!plan->buf[0]) throw std::invalid_argument("plan has no bound buffers");
+    const size_t w = static_cast<size_t>(plan->gx) * 4;
+    const size_t rows = static_cast<size_t>(plan->gy) * static_cast<size_t>(plan->gz);
+    const size_t pitch = plan->storage.row_pitch * 4;
+    float* base = plan->buf[which] + plan->storage.left_pad;
+    if (to_storage) {
+        ck(cudaMemcpy2DAsync(base, pitch, src, w, w, rows,
+                             other_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st),
+           "cudaMemcpy2DAsync(upload)");
+    } else {
+        ck(cudaMemcpy2DAsync(dst, w, base, pitch, w, rows,
+                             other_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st),
+           "cudaMemcpy2DAsync(download)");
+    }
+}
+
+sst_status sst_upload(sst_plan* plan, int which, const float* src, int src_on_device, void* stream) {
+    try {
+        if (!plan || !src) throw std::invalid_argument("null argument");
+        ck(cudaSetDevice(plan->device), "cudaSetDevice");
+        const auto st = static_cast<cudaStream_t>(stream);
+        copy_dense(plan, which, src, nullptr, true, src_on_device != 0, st);
+        // the partner buffer carries the same boundary ring (ping-pong semantics)
+        ck(cudaMemcpyAsync(plan->buf[which ^ 1], plan->buf[which], plan->storage.bytes,
+                           cudaMemcpyDeviceToDevice, st),
+           "cudaMemcpyAsync(ring)");
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_download(sst_plan* plan, int which, float* dst, int dst_on_device, void* stream) {
+    try {
+        if (!plan || !dst) throw std::invalid_argument("null argument");
+        ck(cudaSetDevice(plan->device), "cudaSetDevice");
+        copy_dense(plan, which, nullptr, dst, false, dst_on_device != 0,
+                   static_cast<cudaStream_t>(stream));
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_set_row_window(sst_plan* plan, uint64_t y0, uint64_t y1) {
+    try {
+        if (!plan) throw std::invalid_argument("null plan");
+        plan->y_lo = static_cast<int64_t>(y0);
+        plan->y_hi = static_cast<int64_t>(y1);
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_run_steps(sst_plan* plan, int src, uint64_t steps, void* stream, int* dst_out) {
+    try {
+        if (!plan) throw std::invalid_argument("null plan");
+        if (src < 0 || src > 1) throw std::invalid_argument("buffer index must be 0 or 1");
+        if (!plan->tmap_ok) throw std::invalid_argument("plan has no bound buffers");
+        ck(cudaSetDevice(plan->device), "cudaSetDevice");
+        const auto st = static_cast<cudaStream_t>(stream);
+        int cur = src;
+        for (uint64_t t = 0; t < steps; ++t) {
+            plan->launch(cur, st);
+            cur ^= 1;
+        }
+        if (dst_out) *dst_out = cur;
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_apply_host(sst_plan* plan, const float* h_in, float* h_out, uint64_t steps) {
+    try {
+        if (!plan || !h_in || !h_out) throw std::invalid_argument("null argument");
+        if (!plan->buf[0]) {
+            sst_status s = sst_plan_bind(plan, nullptr, nullptr);
+            if (s != SST_OK) return s;
+        }
+        ck(cudaSetDevice(plan->device), "cudaSetDevice");
+        cudaStream_t st = nullptr;
+        copy_dense(plan, 0, h_in, nullptr, true, false, st);
+        // identical boundary ring in both buffers (device-side copy)
+        ck(cudaMemcpyAsync(plan->buf[1], plan->buf[0], plan->storage.bytes, cudaMemcpyDeviceToDevice, st),
+           "cudaMemcpyAsync(ring)");
+        int cur = 0;
+        for (uint64_t t = 0; t < steps; ++t) {
+            plan->launch(cur, st);
+            cur ^= 1;
+        }
+        copy_dense(plan, cur, nullptr, h_out, false, false, st);
+        ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+}  // extern "C"

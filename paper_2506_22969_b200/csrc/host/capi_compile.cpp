@@ -1,0 +1,213 @@
+// C ABI, compile tier: host-only entry points (no GPU needed). The compile
+// order mirrors the reference pipeline (proj/core/src/pipeline.cpp:56-78, 112):
+// fuse -> choose (r1, r2) -> flatten -> crush -> convert_layout -> compress_24.
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+
+#include "capi_internal.hpp"
+#include "sparstencil.h"
+#include "stensor/hwmodel.hpp"
+#include "stensor/morph.hpp"
+#include "stensor/s24.hpp"
+#include "stensor/sparsify.hpp"
+#include "stensor/spec.hpp"
+
+struct sst_compiled {
+    stensor::StencilSpec spec;
+    std::vector<std::size_t> dims;
+    stensor::Conversion cv;
+    stensor::Sparse24Matrix a2;
+    std::vector<std::uint64_t> col_origin_u64;
+};
+
+namespace sstc {
+
+thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+sst_status from_current_exception() {
+    try {
+        throw;
+    } catch (const std::invalid_argument& e) {
+        set_error(e.what());
+        return SST_ERR_INVALID_ARGUMENT;
+    } catch (const std::out_of_range& e) {
+        set_error(e.what());
+        return SST_ERR_OUT_OF_RANGE;
+    } catch (const std::logic_error& e) {
+        set_error(e.what());
+        return SST_ERR_LOGIC;
+    } catch (const CudaError& e) {
+        set_error(e.what());
+        return e.no_device ? SST_ERR_NO_DEVICE : SST_ERR_CUDA;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return SST_ERR_RUNTIME;
+    } catch (...) {
+        set_error("unknown error");
+        return SST_ERR_RUNTIME;
+    }
+}
+
+}  // namespace sstc
+
+namespace {
+
+stensor::StencilSpec resolve_stencil(const char* text) {
+    if (!text) throw std::invalid_argument("null stencil");
+    const std::string s(text);
+    if (stensor::is_preset(s)) return stensor::stencil_preset(s);
+    if (s.find('=') != std::string::npos) return stensor::parse_stencil_spec(s);
+    throw std::invalid_argument("unknown stencil preset: " + s);
+}
+
+template <class T>
+sst_status copy_out(const std::vector<T>& src, T* buf, size_t cap, size_t* len) {
+    if (len) *len = src.size();
+    if (!buf) return SST_OK;
+    if (cap < src.size()) throw std::invalid_argument("output buffer too small");
+    std::memcpy(buf, src.data(), src.size() * sizeof(T));
+    return SST_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+sst_status sst_compile(const char* stencil, const uint64_t* grid_dims, int ndims, int r1, int r2,
+                       uint64_t fuse, sst_compiled** out) {
+    try {
+        if (!out) throw std::invalid_argument("null output handle");
+        *out = nullptr;
+        auto c = std::make_unique<sst_compiled>();
+        c->spec = resolve_stencil(stencil);
+        if (fuse > 1) c->spec = stensor::fuse_time_steps(c->spec, fuse);
+        if (ndims != c->spec.dims || !grid_dims)
+            throw std::invalid_argument("grid dimensionality does not match stencil");
+        c->dims.assign(grid_dims, grid_dims + ndims);
+        if (r1 <= 0 || r2 <= 0) {
+            const auto ex = stensor::explore_layouts_tcgen05(stensor::hw_preset("b200-sparse"),
+                                                             c->spec, c->dims, 128);
+            r1 = ex.best.r1;
+            r2 = ex.best.r2;
+        }
+        if (c->spec.dims == 1) r2 = 1;
+        const auto flat = stensor::flatten(c->spec, c->dims);
+        const auto morphed = stensor::crush(flat, r1, r2);
+        c->cv = stensor::convert_layout(morphed);
+        c->a2 = stensor::compress_24(c->cv.converted.a);
+        c->col_origin_u64.resize(c->cv.converted.col_origin.size());
+        for (std::size_t i = 0; i < c->col_origin_u64.size(); ++i)
+            c->col_origin_u64[i] = c->cv.converted.col_origin[i] == stensor::npos
+                                       ? UINT64_MAX
+                                       : static_cast<uint64_t>(c->cv.converted.col_origin[i]);
+        *out = c.release();
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+void sst_compiled_destroy(sst_compiled* c) { delete c; }
+
+sst_status sst_compiled_info(const sst_compiled* c, sst_compile_info* info) {
+    try {
+        if (!c || !info) throw std::invalid_argument("null argument");
+        const auto& L = c->cv.converted;
+        *info = sst_compile_info{};
+        info->dims = L.dims;
+        info->k = c->spec.k;
+        info->r1 = L.r1;
+        info->r2 = L.r2;
+        info->m_prime = L.m_prime;
+        info->k_prime = L.k_prime;
+        info->n_prime = L.n_prime;
+        info->cols = L.a.cols;
+        info->p = c->cv.p;
+        info->align_cols = c->cv.align_cols;
+        info->used_blossom = c->cv.used_blossom ? 1 : 0;
+        info->refined = c->cv.matching.refined ? 1 : 0;
+        info->window_w = L.stair.block_size;
+        info->window_h = L.stair.block_count;
+        info->window_d = L.z_factor;
+        for (std::size_t a = 0; a < c->dims.size() && a < 3; ++a) info->grid_dims[a] = c->dims[a];
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_compiled_s24(const sst_compiled* c, uint32_t tag, uint8_t* buf, size_t cap,
+                            size_t* len) {
+    try {
+        if (!c) throw std::invalid_argument("null compiled handle");
+        const std::string bytes = stensor::sparse24_bytes(
+            c->a2, tag ? stensor::Precision::round16 : stensor::Precision::exact64);
+        std::vector<uint8_t> v(bytes.begin(), bytes.end());
+        return copy_out(v, buf, cap, len);
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_compiled_perm(const sst_compiled* c, uint64_t* buf, size_t cap, size_t* len) {
+    try {
+        if (!c) throw std::invalid_argument("null compiled handle");
+        std::vector<uint64_t> v(c->cv.perm.order.begin(), c->cv.perm.order.end());
+        return copy_out(v, buf, cap, len);
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_compiled_col_origin(const sst_compiled* c, uint64_t* buf, size_t cap, size_t* len) {
+    try {
+        if (!c) throw std::invalid_argument("null compiled handle");
+        return copy_out(c->col_origin_u64, buf, cap, len);
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_compiled_matrix(const sst_compiled* c, double* buf, size_t cap, size_t* len) {
+    try {
+        if (!c) throw std::invalid_argument("null compiled handle");
+        return copy_out(c->cv.converted.a.data, buf, cap, len);
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_compiled_plan_desc(const sst_compiled* c, sst_plan_desc* d) {
+    try {
+        if (!c || !d) throw std::invalid_argument("null argument");
+        const auto& L = c->cv.converted;
+        *d = sst_plan_desc{};
+        d->dims = L.dims;
+        d->k = c->spec.k;
+        d->r1 = L.r1;
+        d->r2 = L.r2;
+        for (std::size_t a = 0; a < c->dims.size() && a < 3; ++a) d->grid_dims[a] = c->dims[a];
+        d->rows = c->a2.rows;
+        d->cols = c->a2.logical_cols;
+        d->a_values = c->a2.values.data();
+        d->a_meta = c->a2.meta.data();
+        d->col_origin = c->col_origin_u64.data();
+        d->window_w = L.stair.block_size;
+        d->window_h = L.stair.block_count;
+        d->window_d = L.z_factor;
+        d->precision = SST_PREC_F16;
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+const char* sst_last_error(void) { return sstc::g_last_error.c_str(); }
+
+const char* sst_version(void) { return "sparstencil-b200 0.1.0 (sm_100a, tcgen05.mma.sp kind::f16)"; }
+
+}  // extern "C"

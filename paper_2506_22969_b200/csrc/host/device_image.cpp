@@ -1,0 +1,149 @@
+// Constant-operand images for the tcgen05.mma.sp (kind::f16) stencil kernels.
+//
+// A (sparse, K-major, SWIZZLE_NONE): per 32-wide logical K step a 4 KiB block
+//   of 128 rows x 16 stored halves; core matrices are 8 rows x 16 B,
+//   LBO (K direction) = 128 B, SBO (M direction) = 256 B.
+// E (metadata, TMEM): per K step one 32-bit TMEM column. Lane
+//   L = m0 + 8*k1 + 16*m2 holds, in nibble (g + 4*m1), the 2:4 selector of
+//   A row m0 + 8*m1 + 16*m2, 4-group 4*k1 + g of the step. The nibble is the
+//   reference metadata byte pos0 | pos1 << 2 verbatim (emulator.cpp:74-75);
+//   layout confirmed on B200 by tools/probes/probe_sparse_mma.cu.
+// koff: B''[q, tile] = patch[tile_origin + koff[q]] with koff from the PIT'd
+//   col_origin (layout.cpp:162-188 restated for a shared-memory patch).
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <random>
+#include <stdexcept>
+
+#include "stensor/device_image.hpp"
+#include "stensor/morph.hpp"
+
+namespace stensor {
+
+std::uint16_t f32_to_f16_bits(float f) {
+    std::uint32_t x;
+    std::memcpy(&x, &f, 4);
+    const std::uint32_t sign = (x >> 16) & 0x8000u;
+    std::uint32_t mag = x & 0x7fffffffu;
+    if (mag >= 0x7f800000u) return static_cast<std::uint16_t>(sign | (mag > 0x7f800000u ? 0x7e00u : 0x7c00u));
+    if (mag >= 0x477ff000u) return static_cast<std::uint16_t>(sign | 0x7c00u);  // overflow
+    if (mag < 0x38800000u) {                                                     // subnormal / zero
+        const int e = static_cast<int>(mag >> 23);
+        const int shift = 126 - e;
+        if (shift > 24) return static_cast<std::uint16_t>(sign);
+        const std::uint32_t m = (mag & 0x7fffffu) | 0x800000u;
+        std::uint32_t q = m >> shift;
+        const std::uint32_t rem = m & ((1u << shift) - 1u), halfway = 1u << (shift - 1);
+        if (rem > halfway || (rem == halfway && (q & 1u))) ++q;
+        return static_cast<std::uint16_t>(sign | q);
+    }
+    std::uint32_t h = mag >> 13;
+    const std::uint32_t rem = mag & 0x1fffu;
+    if (rem > 0x1000u || (rem == 0x1000u && (h & 1u))) ++h;
+    return static_cast<std::uint16_t>(sign | (h - (112u << 10)));
+}
+
+namespace {
+
+// distinct addresses per bank among the 32 lanes of one gather LDS
+int bank_degree(const std::array<std::int32_t, 32>& addr) {
+    std::array<std::vector<std::int32_t>, 32> per_bank;
+    for (std::int32_t a : addr) {
+        auto& v = per_bank[static_cast<std::size_t>(((a % 32) + 32) % 32)];
+        if (std::find(v.begin(), v.end(), a) == v.end()) v.push_back(a);
+    }
+    std::size_t worst = 0;
+    for (const auto& v : per_bank) worst = std::max(worst, v.size());
+    return static_cast<int>(worst);
+}
+
+int schedule_cost(const std::vector<std::uint8_t>& order, const std::vector<std::int32_t>& koff,
+                  int* worst_out) {
+    int total = 0, worst = 0;
+    for (std::size_t it = 0; it * 4 < order.size(); ++it) {
+        std::array<std::int32_t, 32> addr{};
+        for (int lane = 0; lane < 32; ++lane)
+            addr[static_cast<std::size_t>(lane)] =
+                koff[static_cast<std::size_t>(order[it * 4 + static_cast<std::size_t>(lane / 8)]) * 8 +
+                     static_cast<std::size_t>(lane % 8)];
+        const int d = bank_degree(addr);
+        total += d;
+        worst = std::max(worst, d);
+    }
+    if (worst_out) *worst_out = worst;
+    return total;
+}
+
+}  // namespace
+
+DeviceImage build_device_image(const BatchGeometry& geo_in, std::size_t rows, std::size_t cols,
+                               const double* values, const std::uint8_t* meta,
+                               const std::size_t* col_origin, std::size_t wv, std::size_t wu) {
+    if (rows != 128) throw std::invalid_argument("device image needs m' = 128 (r1 * r2)");
+    if (cols % 4 != 0) throw std::invalid_argument("A'' column count must be 4-aligned");
+    DeviceImage img;
+    img.geo = geo_in;
+    BatchGeometry& g = img.geo;
+    g.k_pad = static_cast<int>((cols + 31) / 32 * 32);
+    const std::size_t k_pad = static_cast<std::size_t>(g.k_pad), ksteps = k_pad / 32;
+    const std::size_t half_cols = cols / 2, quarter_cols = cols / 4;
+
+    // ---- A image
+    img.a_smem.assign(128 * k_pad / 2, 0);
+    for (std::size_t m = 0; m < 128; ++m)
+        for (std::size_t j = 0; j < half_cols; ++j) {
+            const std::size_t s = j / 16, jj = j % 16;
+            const std::size_t at = s * 2048 + (m / 8) * 128 + (jj / 8) * 64 + (m % 8) * 8 + jj % 8;
+            img.a_smem[at] = f32_to_f16_bits(static_cast<float>(values[m * half_cols + j]));
+        }
+
+    // ---- E words
+    img.e_words.assign(ksteps * 128, 0);
+    for (std::size_t s = 0; s < ksteps; ++s)
+        for (std::size_t m = 0; m < 128; ++m)
+            for (std::size_t gl = 0; gl < 8; ++gl) {
+                const std::size_t grp = s * 8 + gl;
+                const std::uint32_t nib = grp < quarter_cols ? (meta[m * quarter_cols + grp] & 0xfu)
+                                                            : 0x4u;  // padding: canonical {0,1}
+                const std::size_t m0 = m % 8, m1 = (m / 8) % 2, m2 = m / 16;
+                const std::size_t lane = m0 + 8 * (gl / 4) + 16 * m2;
+                img.e_words[s * 128 + lane] |= nib << (4 * ((gl % 4) + 4 * m1));
+            }
+
+    // ---- K-row offsets into the shared-memory patch
+    const std::int32_t plane = g.patch_w * g.patch_h;
+    img.koff.assign(k_pad, 0);  // zero columns read a real (finite) patch cell; A'' is 0 there
+    for (std::size_t q = 0; q < cols; ++q) {
+        const std::size_t j = col_origin[q];
+        if (j == npos) continue;
+        const std::size_t z = j / (wu * wv), u = (j % (wu * wv)) / wv, v = j % wv;
+        img.koff[q] = static_cast<std::int32_t>(z) * plane +
+                      static_cast<std::int32_t>(u) * g.patch_w + static_cast<std::int32_t>(v) +
+                      g.x_shift;
+    }
+
+    // ---- gather schedule: partition 8-row groups into 32-row sweeps with few
+    // shared-memory bank conflicts (deterministic local search)
+    const std::size_t ngroups = k_pad / 8;
+    img.kgroup_order.resize(ngroups);
+    std::iota(img.kgroup_order.begin(), img.kgroup_order.end(), std::uint8_t{0});
+    int best = schedule_cost(img.kgroup_order, img.koff, nullptr);
+    std::mt19937 rng(12345);
+    for (int trial = 0; trial < 4000 && ngroups > 4; ++trial) {
+        const std::size_t a = rng() % ngroups, b = rng() % ngroups;
+        if (a / 4 == b / 4) continue;
+        std::swap(img.kgroup_order[a], img.kgroup_order[b]);
+        const int c = schedule_cost(img.kgroup_order, img.koff, nullptr);
+        if (c <= best)
+            best = c;
+        else
+            std::swap(img.kgroup_order[a], img.kgroup_order[b]);
+    }
+    schedule_cost(img.kgroup_order, img.koff, &img.worst_bank_conflict);
+    return img;
+}
+
+}  // namespace stensor

@@ -1,0 +1,211 @@
+"""Python host mirror of the reference's stencil API over the engine's C ABI.
+
+Reference call (proj/core/include/stensor/stencil.hpp:72):
+    Grid direct_apply(const StencilSpec&, const Grid&, uint64_t steps)
+Engine call (same argument meaning, same valid-region result, same error types):
+    sparse_apply(stencil, grid, steps) -> np.ndarray
+
+`stencil` is a preset name (stencil.cpp:135-159) or a spec document
+(docs/formats.md:3-30). The compile step (flatten -> crush -> convert_layout ->
+compress_24) runs in the C++ host library; every time step runs on the B200
+through tcgen05.mma.sp. There is no CPU execution path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _capi
+from ._capi import check, lib
+
+PRESETS = ["Heat-1D", "1D5P", "Heat-2D", "Box-2D9P", "Star-2D13P", "Box-2D49P", "Heat-3D",
+           "Box-3D27P"]
+
+
+def preset_names() -> list[str]:
+    return list(PRESETS)
+
+
+class Compiled:
+    """Host compile products (reference: flatten/crush/convert_layout/compress_24)."""
+
+    def __init__(self, stencil: str, grid_dims: Sequence[int], r1: int = 0, r2: int = 0,
+                 fuse: int = 1):
+        L = lib()
+        self.grid_dims = [int(d) for d in grid_dims]
+        dims = (C.c_uint64 * len(self.grid_dims))(*self.grid_dims)
+        h = C.c_void_p()
+        check(L.sst_compile(stencil.encode(), dims, len(self.grid_dims), int(r1), int(r2),
+                            int(fuse), C.byref(h)))
+        self._h = h
+        info = _capi.CompileInfo()
+        check(L.sst_compiled_info(self._h, C.byref(info)))
+        self.info = {f: getattr(info, f) for f, _ in _capi.CompileInfo._fields_ if f != "grid_dims"}
+        self.stencil = stencil
+
+    def _fetch(self, fn, ctype, dtype):
+        n = C.c_size_t()
+        check(fn(self._h, None, 0, C.byref(n)))
+        out = np.empty(n.value, dtype=dtype)
+        check(fn(self._h, out.ctypes.data_as(C.c_void_p), n.value, C.byref(n)))
+        return out
+
+    def s24(self, tag: int = 0) -> bytes:
+        L = lib()
+        n = C.c_size_t()
+        check(L.sst_compiled_s24(self._h, tag, None, 0, C.byref(n)))
+        buf = (C.c_uint8 * n.value)()
+        check(L.sst_compiled_s24(self._h, tag, buf, n.value, C.byref(n)))
+        return bytes(buf)
+
+    def perm(self) -> np.ndarray:
+        return self._fetch(lib().sst_compiled_perm, C.c_uint64, np.uint64)
+
+    def col_origin(self) -> np.ndarray:
+        return self._fetch(lib().sst_compiled_col_origin, C.c_uint64, np.uint64)
+
+    def matrix(self) -> np.ndarray:
+        a = self._fetch(lib().sst_compiled_matrix, C.c_double, np.float64)
+        return a.reshape(int(self.info["m_prime"]), int(self.info["cols"]))
+
+    def plan_desc(self) -> _capi.PlanDesc:
+        d = _capi.PlanDesc()
+        check(lib().sst_compiled_plan_desc(self._h, C.byref(d)))
+        return d
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().sst_compiled_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class SparseStencil:
+    """A compiled stencil resident on one B200 (the device-side KernelPlan)."""
+
+    def __init__(self, stencil: str | Compiled, grid_dims: Optional[Sequence[int]] = None,
+                 device: int = 0, r1: int = 16, r2: int = 8, fuse: int = 1):
+        self.compiled = stencil if isinstance(stencil, Compiled) else Compiled(
+            stencil, grid_dims, r1, r2, fuse)
+        self.grid_dims = self.compiled.grid_dims
+        self.k = int(self.compiled.info["k"])
+        self.r = (self.k - 1) // 2
+        desc = self.compiled.plan_desc()
+        h = C.c_void_p()
+        check(lib().sst_plan_create(C.byref(desc), int(device), C.byref(h)))
+        self._h = h
+        self.device = device
+        st = _capi.Storage()
+        check(lib().sst_plan_storage(self._h, C.byref(st)))
+        self.storage = {f: getattr(st, f) for f, _ in _capi.Storage._fields_}
+        self._bufs = None  # keeps caller-provided buffers alive
+
+    # -- buffers -----------------------------------------------------------
+    def bind(self, buf0: int = 0, buf1: int = 0, keepalive=None):
+        """Bind two device buffers (raw pointers) or let the plan allocate (0, 0)."""
+        check(lib().sst_plan_bind(self._h, C.c_void_p(buf0 or None), C.c_void_p(buf1 or None)))
+        self._bufs = keepalive
+
+    def bind_torch(self):
+        """Allocate the ping-pong pair with torch (device memory plumbing only)."""
+        import torch
+        nbytes = int(self.storage["bytes"])
+        dev = torch.device("cuda", self.device)
+        bufs = [torch.empty(nbytes, dtype=torch.uint8, device=dev) for _ in range(2)]
+        self.bind(bufs[0].data_ptr(), bufs[1].data_ptr(), keepalive=bufs)
+        return bufs
+
+    def upload(self, grid, which: int = 0, stream: int = 0):
+        """Dense fp32 grid (numpy host array or torch CUDA tensor) -> buffer `which`."""
+        on_dev, ptr, keep = _pointer(grid)
+        check(lib().sst_upload(self._h, which, C.c_void_p(ptr), int(on_dev), C.c_void_p(stream or None)))
+        return keep
+
+    def download(self, which: int, out=None, stream: int = 0):
+        if out is None:
+            out = np.empty(self.grid_dims, dtype=np.float32)
+        on_dev, ptr, _ = _pointer(out)
+        check(lib().sst_download(self._h, which, C.c_void_p(ptr), int(on_dev), C.c_void_p(stream or None)))
+        return out
+
+    def run(self, steps: int, src: int = 0, stream: int = 0) -> int:
+        dst = C.c_int()
+        check(lib().sst_run_steps(self._h, src, int(steps), C.c_void_p(stream or None), C.byref(dst)))
+        return dst.value
+
+    def set_row_window(self, y0: int, y1: int):
+        check(lib().sst_set_row_window(self._h, int(y0), int(y1)))
+
+    def apply_host(self, grid: np.ndarray, steps: int) -> np.ndarray:
+        """Host buffers in, full-size host buffer out (H2D + steps + D2H)."""
+        g = np.ascontiguousarray(grid, dtype=np.float32)
+        if list(g.shape) != list(self.grid_dims):
+            raise _capi.InvalidArgument("grid shape does not match the compiled grid")
+        out = np.empty_like(g)
+        check(lib().sst_apply_host(self._h, g.ctypes.data_as(C.c_void_p),
+                                   out.ctypes.data_as(C.c_void_p), int(steps)))
+        return out
+
+    def stats(self) -> dict:
+        s = _capi.PlanStats()
+        check(lib().sst_plan_stats_get(self._h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in _capi.PlanStats._fields_}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().sst_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _pointer(arr):
+    """(on_device, address, keepalive) for numpy arrays and torch tensors."""
+    if isinstance(arr, np.ndarray):
+        if arr.dtype != np.float32 or not arr.flags["C_CONTIGUOUS"]:
+            raise _capi.InvalidArgument("expected a C-contiguous float32 array")
+        return False, arr.ctypes.data, arr
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        torch = None
+    if torch is not None and isinstance(arr, torch.Tensor):
+        if arr.dtype != torch.float32 or not arr.is_contiguous():
+            raise _capi.InvalidArgument("expected a contiguous float32 tensor")
+        return arr.is_cuda, arr.data_ptr(), arr
+    raise _capi.InvalidArgument(f"unsupported buffer type {type(arr)!r}")
+
+
+def valid_core(full: np.ndarray, steps: int, r: int) -> np.ndarray:
+    """Crop a fixed-size result to the reference's valid region after `steps`."""
+    c = steps * r
+    sl = tuple(slice(c, n - c) for n in full.shape)
+    return full[sl]
+
+
+def sparse_apply(stencil: str, grid: np.ndarray, steps: int, device: int = 0) -> np.ndarray:
+    """Drop-in for stensor::direct_apply (stencil.hpp:72): valid-region result
+    (extent N - steps*(k-1) per axis) computed on the B200."""
+    if steps < 1:
+        raise _capi.InvalidArgument("steps must be >= 1")
+    g = np.asarray(grid)
+    eng = SparseStencil(stencil, list(g.shape), device=device)
+    try:
+        for n in g.shape:
+            if n < eng.k + (steps - 1) * (eng.k - 1):
+                raise _capi.InvalidArgument("grid smaller than kernel")
+        full = eng.apply_host(g.astype(np.float32), steps)
+        return valid_core(full, steps, eng.r).astype(np.float64)
+    finally:
+        eng.close()
