@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 SparStencil hot path (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1]): Box-2D9P, 8192 x 8192 fp32 grid, 1000 time
+steps, synthetic dyadic input (random_grid, seed 1), 2:4-sparse tcgen05.mma.sp
+(f16 operands, f32 accumulate, f32 storage). A bench *step* is one time step:
+one pass of the compiled stencil over the whole grid (one kernel launch).
+Default --steps 1000 times the config's full 1000-step run.
+
+  value      GStencil/s = steps * prod(N) / t (Eq. 12, stencil.cpp:349-359),
+             grid resident in HBM, CUDA events on the launch stream, max over ranks
+  e2e        the same metric through the public API from HOST memory: one
+             sst_apply_host call = H2D of the grid + `steps` time steps + D2H
+  roofline   dominant kernel vs measured HBM copy bandwidth (8 B per update)
+  cpu_baseline  the reference's own direct_apply (oracle/_ref, built from the
+             reference sources) on the host cores, bounded sample
+
+N > 1 (torchrun): weak scaling, each rank owns an 8192-row slab of a
+(8192*N) x 8192 global grid; halo rows are exchanged with NCCL every step.
+
+--impl reference: the reference CPU implementation (oracle/_ref) on the host
+cores, same metric; each step is one time step over a bounded row band.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+CONFIGS = {
+    # name: (stencil, dims, default time steps)
+    "box2d": ("Box-2D9P", (8192, 8192), 1000),
+    "heat2d": ("Heat-2D", (4096, 4096), 100),
+    "star2d": ("Star-2D13P", (16384, 16384), 100),
+    "heat3d": ("Heat-3D", (512, 512, 512), 100),
+    "box3d": ("Box-3D27P", (512, 512, 512), 100),
+    "box3d1024": ("Box-3D27P", (1024, 1024, 1024), 100),
+}
+METRIC = "GStencil/s per stencil at 1/2/4/8 B200; % of HBM & sparse-TC roofline"
+
+
+def _peaks():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def _dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True,
+                                         text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def _load_traffic(cfg_name):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    p = REPO / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get(cfg_name)
+        except Exception:
+            return None
+    return None
+
+
+def cpu_baseline(stencil, dims, budget_s=12.0):
+    """Reference direct_apply (oracle/_ref) on all host cores, bounded sample."""
+    import oracle
+
+    threads = os.cpu_count() or 1
+    if oracle.ref_available():
+        kind = "reference"
+        fn = lambda g: oracle.ref_direct_apply_slabs(stencil, g, threads)  # noqa: E731
+    else:  # the C restatement (single thread) when the reference .so is absent
+        kind, threads = "port", 1
+        fn = lambda g: oracle.direct_apply(stencil, g, 1)  # noqa: E731
+    # a band of rows of the same grid (full row length), one time step per call
+    band = list(dims)
+    band[0] = min(dims[0], max(64, int(4_000_000 // int(np.prod(dims[1:])))))
+    g = oracle.random_grid(band, seed=1)
+    fn(g)  # warm
+    n, t0 = 0, time.perf_counter()
+    while True:
+        fn(g)
+        n += 1
+        if time.perf_counter() - t0 > budget_s or n >= 200:
+            break
+    dt = time.perf_counter() - t0
+    cells = n * int(np.prod(band))
+    return {"value": cells / dt / 1e9, "unit": "GStencil/s", "cores": threads, "kind": kind,
+            "sample": f"{n} x one time step of {stencil} on a {'x'.join(map(str, band))} band "
+                      f"of the {'x'.join(map(str, dims))} grid ({dt:.1f} s)"}
+
+
+def run_reference(args, cfg):
+    stencil, dims, tsteps = cfg
+    ws, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    import oracle
+
+    threads = os.cpu_count() or 1
+    kind = "reference" if oracle.ref_available() else "port"
+    band = list(dims)
+    band[0] = min(dims[0], max(32, int(2_000_000 // int(np.prod(dims[1:])))))
+    g = oracle.random_grid(band, seed=1)
+    fn = (lambda: oracle.ref_direct_apply_slabs(stencil, g, threads)) if kind == "reference" \
+        else (lambda: oracle.direct_apply(stencil, g, 1))
+    if kind == "port":
+        threads = 1
+    for _ in range(args.warmup):
+        fn()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        fn()
+    dt = time.perf_counter() - t0
+    val = args.steps * int(np.prod(band)) / dt / 1e9
+    line = {"metric": METRIC, "value": val, "unit": "GStencil/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (random_grid seed 1, dyadic)", "impl": "reference",
+            "config": {"workload": f"{stencil} {'x'.join(map(str, dims))}, one time step per "
+                                   f"bench step over a {'x'.join(map(str, band))} row band",
+                       "stencil": stencil, "grid": list(dims)},
+            "cpu_baseline": {"value": val, "unit": "GStencil/s", "cores": threads, "kind": kind,
+                             "sample": f"{args.steps} time steps over a {'x'.join(map(str, band))} band"},
+            "e2e": {"value": val, "unit": "GStencil/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_engine(args, cfg, cfg_name):
+    import torch
+
+    from paper_2506_22969_b200 import SparseStencil
+
+    stencil, dims, _ = cfg
+    ws, rank, local = _dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    # weak scaling: each rank owns a slab of `dims` rows (plus halo rows)
+    from paper_2506_22969_b200.multigpu import SlabStencil
+
+    eng = SlabStencil(stencil, dims, rank=rank, world=ws, device=local)
+    grid = eng.make_local_input(seed=1)  # dense fp32 torch tensor on the device
+    eng.load(grid)
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(args.warmup):
+        eng.step(1)
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = eng.launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    ev0.record(stream)
+    eng.step(args.steps)
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    launches = eng.launches() - launches0
+    if ws > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    cells_global = int(np.prod(dims)) * ws
+    value = args.steps * cells_global / (ms / 1e3) / 1e9
+
+    # roofline of the dominant kernel: 8 B per interior update (read 4 + write 4)
+    interior = eng.interior_cells()
+    t_launch = ms / 1e3 / max(1, launches) * (launches / max(1, args.steps * eng.kernels_per_step()))
+    t_kernel = ms / 1e3 / args.steps / eng.kernels_per_step() * eng.kernels_per_step()
+    alg_bytes = 8.0 * interior
+    peak, peak_kind = _peaks()
+    achieved = alg_bytes / t_kernel / 1e9
+    traffic = _load_traffic(cfg_name)
+
+    # e2e through the public API from host memory (rank-local slab)
+    e2e = None
+    if not args.no_e2e:
+        host = grid.cpu().numpy()
+        e2e_steps = args.e2e_steps or args.steps
+        eng.apply_host(host, min(e2e_steps, 3))  # warm
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        eng.apply_host(host, e2e_steps)
+        dt = time.perf_counter() - t0
+        if ws > 1:
+            t = torch.tensor([dt], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        nbytes = int(host.nbytes)
+        e2e = {"value": e2e_steps * cells_global / dt / 1e9, "unit": "GStencil/s",
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "step": f"one sst_apply_host call = H2D + {e2e_steps} time steps + D2H"}
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None if (ws > 1 or args.no_cpu) else cpu_baseline(stencil, dims)
+    line = {
+        "metric": METRIC, "value": value, "unit": "GStencil/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+        "data": "synthetic (random_grid seed 1: dyadic values in [0,1))",
+        "config": {"workload": f"{stencil} {'x'.join(map(str, dims))} per GPU, "
+                               f"{args.steps} time steps (one bench step = one time step)",
+                   "stencil": stencil, "grid_per_gpu": list(dims), "time_steps": args.steps,
+                   "storage": "fp32", "operands": "f16 (tcgen05.mma.sp kind::f16), f32 accumulate",
+                   "layout": "(r1, r2) = (16, 8), m' = 128",
+                   "l2": "inputs larger than L2 (grid > 126 MB)" if cells_global * 4 > 126e6
+                         else "grid fits in L2: no flush between steps (state it)",
+                   "parallelism": f"slab{ws}" if ws > 1 else "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "kernel": "sst::stencil_step_kernel"},
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    ap.add_argument("--config", default="box2d", choices=sorted(CONFIGS))
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.steps is None:
+        args.steps = cfg[2]
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_engine(args, cfg, args.config)
+
+
+if __name__ == "__main__":
+    main()

@@ -130,6 +130,7 @@ SST_API sst_status sst_plan_storage(const sst_plan* plan, sst_storage* st);
 typedef struct sst_plan_stats {
     int32_t k_pad, k_steps, tiles_x, tiles_y, patch_w, patch_h, patch_planes;
     int32_t worst_bank_conflict;
+    int32_t patch_stages;  /* depth of the TMA patch ring */
     int32_t smem_bytes, ctas, batches;
     uint64_t launches;     /* kernel launches issued by this plan so far */
 } sst_plan_stats;
@@ -156,6 +157,9 @@ SST_API sst_status sst_set_row_window(sst_plan* plan, uint64_t y0, uint64_t y1);
 SST_API sst_status sst_apply_host(sst_plan* plan, const float* h_in, float* h_out, uint64_t steps);
 
 /* ----------------------------------------------------------------- misc */
+/* Synthetic input: stensor::random_grid (stencil.hpp:84-85; mt19937_64(seed),
+ * (x & 0xff) / 256, dyadic and exact in fp32), written as fp32. */
+SST_API sst_status sst_random_grid(int ndims, const uint64_t* dims, uint64_t seed, float* out);
 SST_API const char* sst_last_error(void);
 SST_API int sst_device_count(void);
 SST_API const char* sst_version(void);

@@ -21,7 +21,8 @@ EXPORTED = [
     "sst_compiled_perm", "sst_compiled_col_origin", "sst_compiled_matrix",
     "sst_compiled_plan_desc", "sst_plan_create", "sst_plan_destroy", "sst_plan_storage",
     "sst_plan_stats_get", "sst_plan_bind", "sst_upload", "sst_download", "sst_run_steps",
-    "sst_set_row_window", "sst_apply_host", "sst_last_error", "sst_device_count", "sst_version",
+    "sst_set_row_window", "sst_apply_host", "sst_random_grid", "sst_last_error",
+    "sst_device_count", "sst_version",
 ]
 
 
@@ -80,6 +81,7 @@ class PlanStats(C.Structure):
     _fields_ = [("k_pad", C.c_int32), ("k_steps", C.c_int32), ("tiles_x", C.c_int32),
                 ("tiles_y", C.c_int32), ("patch_w", C.c_int32), ("patch_h", C.c_int32),
                 ("patch_planes", C.c_int32), ("worst_bank_conflict", C.c_int32),
+                ("patch_stages", C.c_int32),
                 ("smem_bytes", C.c_int32), ("ctas", C.c_int32), ("batches", C.c_int32),
                 ("launches", C.c_uint64)]
 
@@ -116,6 +118,7 @@ def lib() -> C.CDLL:
         "sst_run_steps": (i32, [P, i32, u64, P, C.POINTER(i32)]),
         "sst_set_row_window": (i32, [P, u64, u64]),
         "sst_apply_host": (i32, [P, P, P, u64]),
+        "sst_random_grid": (i32, [i32, C.POINTER(u64), u64, P]),
         "sst_last_error": (C.c_char_p, []),
         "sst_device_count": (i32, []),
         "sst_version": (C.c_char_p, []),

@@ -47,11 +47,46 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-template <int DIMS, int TXB, int TYB>
-void configure_kernel(int smem) {
-    ck(cudaFuncSetAttribute(sst::stencil_step_kernel<DIMS, TXB, TYB>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-       "cudaFuncSetAttribute");
+// One compiled instantiation of the step kernel: (dims, tile rows per batch,
+// patch pipeline depth). Plans pick the deepest variant that fits in smem.
+struct Variant {
+    int dims, tyb, np;
+    sst::SmemLayout (*layout)(int nks, int k_pad, int pw, int ph, int planes);
+    void (*configure)(int smem);
+    void (*launch)(int grid, int smem, cudaStream_t st, const CUtensorMap& tm,
+                   const sst::StepParams& p);
+};
+
+template <int D, int TYB, int NP>
+Variant make_variant() {
+    Variant v{};
+    v.dims = D;
+    v.tyb = TYB;
+    v.np = NP;
+    v.layout = [](int nks, int k_pad, int pw, int ph, int planes) {
+        return sst::smem_layout<8, TYB, NP>(nks, k_pad, pw, ph, planes);
+    };
+    v.configure = [](int smem) {
+        ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, 8, TYB, NP>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+           "cudaFuncSetAttribute");
+    };
+    v.launch = [](int grid, int smem, cudaStream_t st, const CUtensorMap& tm,
+                  const sst::StepParams& p) {
+        sst::stencil_step_kernel<D, 8, TYB, NP><<<grid, sst::kThreads, smem, st>>>(tm, p);
+    };
+    return v;
+}
+
+// preference order per dimensionality: deepest TMA pipeline first
+const Variant* variants(int& n) {
+    static const Variant v[] = {
+        make_variant<2, 8, 4>(), make_variant<2, 8, 3>(), make_variant<2, 4, 4>(),
+        make_variant<2, 8, 2>(), make_variant<2, 4, 2>(),
+        make_variant<3, 2, 4>(), make_variant<3, 2, 3>(), make_variant<3, 2, 2>(),
+    };
+    n = static_cast<int>(sizeof(v) / sizeof(v[0]));
+    return v;
 }
 
 }  // namespace
@@ -62,6 +97,7 @@ struct sst_plan {
     int gx = 0, gy = 1, gz = 1;
     stensor::DeviceImage img;
     int tiles_y = 8;
+    const Variant* variant = nullptr;
     sst_storage storage{};
     int smem = 0, num_sms = 0;
     // device constants
@@ -88,8 +124,6 @@ struct sst_plan {
             cudaFree(buf[1]);
         }
     }
-
-    int64_t interior_rows() const { return (dims == 3 ? gy : gy) - 2 * r; }
 
     void make_tmaps() {
         const int g = img.geo.patch_planes;
@@ -126,13 +160,19 @@ struct sst_plan {
         p.gy = gy;
         p.gz = gz;
         p.r = r;
-        const int64_t rows = gy - 2 * r;
-        p.y_lo = static_cast<int32_t>(y_hi > y_lo ? y_lo : 0);
-        p.y_hi = static_cast<int32_t>(y_hi > y_lo ? std::min<int64_t>(y_hi, rows) : rows);
+        const int64_t slow = (dims == 3 ? gz : gy) - 2 * r;  // interior extent, slowest axis
+        p.slow_lo = static_cast<int32_t>(y_hi > y_lo ? std::min<int64_t>(y_lo, slow) : 0);
+        p.slow_hi = static_cast<int32_t>(y_hi > y_lo ? std::min<int64_t>(y_hi, slow) : slow);
+        p.y_end = gy - 2 * r;
         const int bw = img.geo.tiles_x * sst::kTileW, bh = tiles_y * sst::kTileH;
         p.nbx = (gx - 2 * r + bw - 1) / bw;
-        p.nby = (p.y_hi - p.y_lo + bh - 1) / bh;
-        p.nbz = dims == 3 ? gz - 2 * r : 1;
+        if (dims == 2) {
+            p.nby = (p.slow_hi - p.slow_lo + bh - 1) / bh;
+            p.nbz = 1;
+        } else {
+            p.nby = (p.y_end + bh - 1) / bh;
+            p.nbz = std::max(0, p.slow_hi - p.slow_lo);
+        }
         p.nbatch = p.nbx * p.nby * p.nbz;
         p.k_pad = img.geo.k_pad;
         p.nks = img.geo.k_pad / 32;
@@ -146,10 +186,7 @@ struct sst_plan {
         const sst::StepParams p = step_params(src);
         if (p.nbatch <= 0) return;
         const int grid = std::min(p.nbatch, num_sms);
-        if (dims == 2)
-            sst::stencil_step_kernel<2, 8, 8><<<grid, sst::kThreads, smem, st>>>(tmap[src], p);
-        else
-            sst::stencil_step_kernel<3, 8, 2><<<grid, sst::kThreads, smem, st>>>(tmap[src], p);
+        variant->launch(grid, smem, st, tmap[src], p);
         ck(cudaGetLastError(), "kernel launch");
         ++launches;
     }
@@ -188,45 +225,47 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
         if (P->gx < d->k || P->gy < d->k || P->gz < (d->dims == 3 ? d->k : 1))
             throw std::invalid_argument("grid smaller than kernel");
 
+        // storage: interior column r lands on a 16-byte boundary
+        const uint64_t lp = (4 - static_cast<uint64_t>(P->r) % 4) % 4;
+        int max_smem = 0;
+        ck(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device),
+           "cudaDeviceGetAttribute");
+        ck(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, device),
+           "cudaDeviceGetAttribute");
+        const int k_pad = static_cast<int>((d->cols + 31) / 32 * 32);
         stensor::BatchGeometry geo;
         geo.dims = d->dims;
         geo.k = d->k;
         geo.tiles_x = 8;
-        geo.tiles_y = d->dims == 2 ? 8 : 2;
-        P->tiles_y = geo.tiles_y;
         geo.patch_planes = d->dims == 3 ? d->k : 1;
-        geo.patch_h = static_cast<int>(d->window_h) + sst::kTileH * (geo.tiles_y - 1);
-        // storage: interior column r lands on a 16-byte boundary
-        const uint64_t lp = (4 - static_cast<uint64_t>(P->r) % 4) % 4;
         // the patch is loaded from the 16-byte aligned storage column X0, i.e.
         // lp cells left of the window origin (TMA box starts must be aligned)
         geo.x_shift = static_cast<int>(lp);
         geo.patch_w = static_cast<int>(sst::align_up(
             static_cast<uint32_t>(lp + d->window_w + sst::kTileW * (geo.tiles_x - 1)), 4));
+        int nvar = 0;
+        const Variant* vars = variants(nvar);
+        for (int i = 0; i < nvar && !P->variant; ++i) {
+            if (vars[i].dims != d->dims) continue;
+            const int ph = static_cast<int>(d->window_h) + sst::kTileH * (vars[i].tyb - 1);
+            const sst::SmemLayout L = vars[i].layout(k_pad / 32, k_pad, geo.patch_w, ph, geo.patch_planes);
+            const int need = static_cast<int>(L.total) + 1024;  // slack for the 1 KiB base alignment
+            if (need > max_smem || ph > 256) continue;
+            P->variant = &vars[i];
+            P->smem = need;
+            geo.tiles_y = vars[i].tyb;
+            geo.patch_h = ph;
+        }
+        if (!P->variant)
+            throw std::invalid_argument("stencil too wide for one CTA's shared memory");
+        P->tiles_y = geo.tiles_y;
         std::vector<std::size_t> origin(d->cols);
         for (std::size_t i = 0; i < d->cols; ++i)
             origin[i] = d->col_origin[i] == UINT64_MAX ? stensor::npos
                                                        : static_cast<std::size_t>(d->col_origin[i]);
         P->img = stensor::build_device_image(geo, d->rows, d->cols, d->a_values, d->a_meta,
                                              origin.data(), d->window_w, d->window_h);
-        const auto& G = P->img.geo;
-        const int nks = G.k_pad / 32;
-        const sst::SmemLayout L =
-            d->dims == 2 ? sst::smem_layout<8, 8>(nks, G.k_pad, G.patch_w, G.patch_h, G.patch_planes)
-                         : sst::smem_layout<8, 2>(nks, G.k_pad, G.patch_w, G.patch_h, G.patch_planes);
-        P->smem = static_cast<int>(L.total) + 1024;  // slack for the 1 KiB base alignment
-        int max_smem = 0;
-        ck(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device),
-           "cudaDeviceGetAttribute");
-        if (P->smem > max_smem)
-            throw std::invalid_argument("stencil too wide for one CTA's shared memory (" +
-                                        std::to_string(P->smem) + " B)");
-        ck(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, device),
-           "cudaDeviceGetAttribute");
-        if (d->dims == 2)
-            configure_kernel<2, 8, 8>(P->smem);
-        else
-            configure_kernel<3, 8, 2>(P->smem);
+        P->variant->configure(P->smem);
 
         P->storage.left_pad = lp;
         P->storage.row_pitch = (lp + static_cast<uint64_t>(P->gx) + 3) / 4 * 4;
@@ -278,6 +317,7 @@ sst_status sst_plan_stats_get(const sst_plan* plan, sst_plan_stats* s) {
         s->patch_h = G.patch_h;
         s->patch_planes = G.patch_planes;
         s->worst_bank_conflict = plan->img.worst_bank_conflict;
+        s->patch_stages = plan->variant->np;
         s->smem_bytes = plan->smem;
         const sst::StepParams p = plan->step_params(0);
         s->batches = p.nbatch;
@@ -357,8 +397,9 @@ sst_status sst_download(sst_plan* plan, int which, float* dst, int dst_on_device
     try {
         if (!plan || !dst) throw std::invalid_argument("null argument");
         ck(cudaSetDevice(plan->device), "cudaSetDevice");
-        copy_dense(plan, which, nullptr, dst, false, dst_on_device != 0,
-                   static_cast<cudaStream_t>(stream));
+        const auto st = static_cast<cudaStream_t>(stream);
+        copy_dense(plan, which, nullptr, dst, false, dst_on_device != 0, st);
+        if (!dst_on_device) ck(cudaStreamSynchronize(st), "cudaStreamSynchronize(download)");
         return SST_OK;
     } catch (...) {
         return sstc::from_current_exception();

@@ -4,16 +4,17 @@
 // output_position, layout.cpp:190-209) becomes, per CTA batch of
 // TXB x TYB output tiles (tile = 16 x 8 outputs, D row m = dx*8 + dy):
 //
-//   warp 0      TMA producer: grid patch (+halo, zero-filled outside) -> smem
+//   warp 0      TMA producer: grid patch (+halo, zero-filled outside) -> smem,
+//               NP-deep ring so several patches are in flight per SM
 //   warps 2-5   gather: B''[q, tile] = patch[tile_origin + koff[q]] (the
 //               memory map of layout.cpp:162-188), fp32 -> fp16 (RNE, the
 //               reference round16 rounding), into the UMMA MN-major operand
 //   warp 1      MMA issuer: tcgen05.mma.sp.cta_group::1.kind::f16, A'' from
 //               smem (compressed, K-major), metadata from TMEM, D in TMEM
-//   warps 6-9   epilogue: tcgen05.ld -> masked stores of the interior outputs
+//   warps 6-9   epilogue: tcgen05.ld -> stores of the interior outputs
 //
-// Double-buffered patch / B operand / TMEM accumulator, mbarrier handshakes
-// between roles, persistent CTAs (one per SM) striding over batches.
+// mbarrier handshakes between roles, double-buffered B operand and TMEM
+// accumulator, persistent CTAs (one per SM) striding over batches.
 #pragma once
 
 #include <cuda.h>
@@ -41,19 +42,20 @@ struct StepParams {
     int32_t left_pad;
     int32_t gx, gy, gz;        // logical extents
     int32_t r;                 // radius
-    int32_t y_lo, y_hi;        // interior output row window [y_lo, y_hi) (interior coords)
+    int32_t slow_lo, slow_hi;  // window over the slowest axis (y in 2D, z in 3D), interior coords
+    int32_t y_end;             // interior rows (gy - 2r)
     int32_t nbx, nby, nbz, nbatch;
     int32_t k_pad, nks;
     int32_t patch_w, patch_h, patch_planes;
 };
 
 struct SmemLayout {
-    uint32_t a, b0, b1, p0, p1, koff, korder, bars, tmem_slot, total;
+    uint32_t a, b, b_stride, p, p_stride, koff, korder, bars, tmem_slot, total;
 };
 
 __host__ __device__ inline uint32_t align_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
-template <int TXB, int TYB>
+template <int TXB, int TYB, int NP>
 __host__ __device__ inline SmemLayout smem_layout(int nks, int k_pad, int patch_w, int patch_h,
                                                   int planes) {
     constexpr int N = TXB * TYB;
@@ -61,59 +63,58 @@ __host__ __device__ inline SmemLayout smem_layout(int nks, int k_pad, int patch_
     uint32_t o = 0;
     L.a = o;
     o += static_cast<uint32_t>(nks) * 4096u;
-    const uint32_t bbytes = static_cast<uint32_t>(k_pad) * N * 2u;
-    L.b0 = o = align_up(o, 1024);
-    o += bbytes;
-    L.b1 = o = align_up(o, 1024);
-    o += bbytes;
-    const uint32_t pbytes = static_cast<uint32_t>(patch_w * patch_h * planes) * 4u;
-    L.p0 = o = align_up(o, 128);
-    o += pbytes;
-    L.p1 = o = align_up(o, 128);
-    o += pbytes;
+    L.b_stride = align_up(static_cast<uint32_t>(k_pad) * N * 2u, 1024);
+    L.b = o = align_up(o, 1024);
+    o += 2 * L.b_stride;
+    L.p_stride = align_up(static_cast<uint32_t>(patch_w * patch_h * planes) * 4u, 128);
+    L.p = o = align_up(o, 128);
+    o += NP * L.p_stride;
     L.koff = o = align_up(o, 16);
     o += static_cast<uint32_t>(k_pad) * 4u;
     L.korder = o = align_up(o, 16);
     o += static_cast<uint32_t>(k_pad / 8);
     L.bars = o = align_up(o, 8);
-    o += 12 * 8;
+    o += (2 * NP + 8) * 8;
     L.tmem_slot = o;
     o += 16;
     L.total = align_up(o, 128);
     return L;
 }
 
-template <int DIMS, int TXB, int TYB>
+template <int DIMS, int TXB, int TYB, int NP>
 __global__ void __launch_bounds__(kThreads, 1)
     stencil_step_kernel(const __grid_constant__ CUtensorMap tmap_in, const StepParams p) {
     static_assert(TXB == 8, "gather assumes 8 x-tiles per MMA column group");
+    static_assert(TYB % 4 == 0 || TYB < 4, "gather warps split the tile rows");
     constexpr int N = TXB * TYB;
     static_assert(N % 16 == 0 && N <= 128, "UMMA N for M=128");
     using namespace ptx;
 
     extern __shared__ __align__(1024) uint8_t smem[];
-    const SmemLayout L = smem_layout<TXB, TYB>(p.nks, p.k_pad, p.patch_w, p.patch_h, p.patch_planes);
+    const SmemLayout L = smem_layout<TXB, TYB, NP>(p.nks, p.k_pad, p.patch_w, p.patch_h, p.patch_planes);
     uint8_t* sA = smem + L.a;
-    uint8_t* sB[2] = {smem + L.b0, smem + L.b1};
-    float* sP[2] = {reinterpret_cast<float*>(smem + L.p0), reinterpret_cast<float*>(smem + L.p1)};
+    uint8_t* sB = smem + L.b;     // 2 stages of b_stride bytes
+    uint8_t* sP = smem + L.p;     // NP stages of p_stride bytes
     int32_t* sKoff = reinterpret_cast<int32_t*>(smem + L.koff);
     uint8_t* sKorder = smem + L.korder;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
-    uint64_t* patch_full = bars + 0;
-    uint64_t* patch_empty = bars + 2;
-    uint64_t* b_full = bars + 4;
-    uint64_t* b_empty = bars + 6;
-    uint64_t* d_full = bars + 8;
-    uint64_t* d_empty = bars + 10;
+    uint64_t* patch_full = bars;
+    uint64_t* patch_empty = bars + NP;
+    uint64_t* b_full = bars + 2 * NP;
+    uint64_t* b_empty = b_full + 2;
+    uint64_t* d_full = b_full + 4;
+    uint64_t* d_empty = b_full + 6;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem_slot);
 
     const int warp = threadIdx.x / 32;
     const uint32_t lane = lane_id();
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < NP; ++s) {
             mbar_init(&patch_full[s], 1);
             mbar_init(&patch_empty[s], kGatherWarps);
+        }
+        for (int s = 0; s < 2; ++s) {
             mbar_init(&b_full[s], kGatherWarps);
             mbar_init(&b_empty[s], 1);
             mbar_init(&d_full[s], 1);
@@ -123,8 +124,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch_desc(&tmap_in);
     }
     if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
-    // constant operands: A'' image, gather tables
-    {
+    {  // constant operands: A'' image, gather tables
         const int n16 = p.nks * 4096 / 16;
         uint4* dstA = reinterpret_cast<uint4*>(sA);
         for (int i = threadIdx.x; i < n16; i += kThreads) dstA[i] = p.a_img[i];
@@ -152,8 +152,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nbx = p.nbx, nby = p.nby;
     auto batch_coords = [&](int b, int& X0, int& Y0, int& Z0) {
         X0 = (b % nbx) * (TXB * kTileW);
-        Y0 = p.y_lo + ((b / nbx) % nby) * (TYB * kTileH);
-        Z0 = b / (nbx * nby);
+        Y0 = ((b / nbx) % nby) * (TYB * kTileH) + (DIMS == 2 ? p.slow_lo : 0);
+        Z0 = b / (nbx * nby) + (DIMS == 3 ? p.slow_lo : 0);
     };
 
     if (warp == 0) {
@@ -162,24 +162,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t pbytes = static_cast<uint32_t>(p.patch_w * p.patch_h * p.patch_planes) * 4u;
             int it = 0;
             for (int b = blockIdx.x; b < p.nbatch; b += gridDim.x, ++it) {
-                const int s = it & 1;
-                const uint32_t ph = (it >> 1) & 1;
+                const int s = it % NP;
+                const uint32_t ph = (it / NP) & 1;
                 int X0, Y0, Z0;
                 batch_coords(b, X0, Y0, Z0);
                 mbar_wait(&patch_empty[s], ph ^ 1);
                 mbar_arrive_expect_tx(&patch_full[s], pbytes);
                 // storage column X0 is 16-byte aligned (TMA requirement); the
                 // window origin sits left_pad cells into the patch (koff has it)
+                void* dst = sP + s * L.p_stride;
                 if (DIMS == 2)
-                    tma_load_2d(sP[s], &tmap_in, &patch_full[s], X0, Y0);
+                    tma_load_2d(dst, &tmap_in, &patch_full[s], X0, Y0);
                 else
-                    tma_load_3d(sP[s], &tmap_in, &patch_full[s], X0, Y0, Z0);
+                    tma_load_3d(dst, &tmap_in, &patch_full[s], X0, Y0, Z0);
             }
         }
     } else if (warp == 1) {
         // -------------------------------------------------------- MMA issuer
         const uint32_t idesc = make_idesc_f16(128, N, true, 0, 1);
         const uint32_t b_sbo = static_cast<uint32_t>(p.k_pad) * 16u;
+        const uint32_t a0 = smem_u32(sA);
         int it = 0;
         for (int b = blockIdx.x; b < p.nbatch; b += gridDim.x, ++it) {
             const int s = it & 1;
@@ -188,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&d_empty[s], ph ^ 1);
             tc_fence_after();
             if (elect_one()) {
-                const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB[s]);
+                const uint32_t b0 = smem_u32(sB + s * L.b_stride);
                 for (int ks = 0; ks < p.nks; ++ks) {
                     const uint64_t ad = make_smem_desc(a0 + ks * 4096u, 128, 256);
                     const uint64_t bd = make_smem_desc(b0 + ks * 512u, 128, b_sbo);
@@ -203,40 +205,49 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp < kGatherWarp0 + kGatherWarps) {
         // ------------------------------------------------------------ gather
+        // warp gw handles tile rows g = gw, gw + 4, ... for every K sweep j;
+        // lane -> one B'' row k of the sweep, 8 tiles along x per 16-B store
         const int gw = warp - kGatherWarp0;
-        const int items = p.nks * TYB;
+        const uint32_t row_stride = static_cast<uint32_t>(kTileH * p.patch_w) * 4u;
         int it = 0;
         for (int b = blockIdx.x; b < p.nbatch; b += gridDim.x, ++it) {
+            const int ps = it % NP;
+            const uint32_t pph = (it / NP) & 1;
             const int s = it & 1;
             const uint32_t ph = (it >> 1) & 1;
-            mbar_wait(&patch_full[s], ph);
+            mbar_wait(&patch_full[ps], pph);
             mbar_wait(&b_empty[s], ph ^ 1);
-            const float* patch = sP[s];
-            const uint32_t bbase = smem_u32(sB[s]);
-            for (int item = gw; item < items; item += kGatherWarps) {
-                const int j = item / TYB, g = item % TYB;
-                const int kg = sKorder[4 * j + static_cast<int>(lane / 8)];
-                const int k = kg * 8 + static_cast<int>(lane % 8);
-                const float* src = patch + sKoff[k] + g * kTileH * p.patch_w;
-                float v[8];
+            const uint32_t pbase = smem_u32(sP + ps * L.p_stride);
+            const uint32_t bbase = smem_u32(sB + s * L.b_stride);
+#pragma unroll 1
+            for (int j = 0; j < p.nks; ++j) {
+                const int k = sKorder[4 * j + static_cast<int>(lane / 8)] * 8 + static_cast<int>(lane % 8);
+                const uint32_t src0 = pbase + static_cast<uint32_t>(sKoff[k]) * 4u;
+                const uint32_t dst0 = bbase + static_cast<uint32_t>(k) * 16u;
 #pragma unroll
-                for (int t = 0; t < 8; ++t) v[t] = src[t * kTileW];
-                uint32_t h[4];
+                for (int g = gw; g < TYB; g += kGatherWarps) {
+                    const uint32_t src = src0 + static_cast<uint32_t>(g) * row_stride;
+                    float v[8];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const __half2 hv = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
-                    h[i] = *reinterpret_cast<const uint32_t*>(&hv);
+                    for (int t = 0; t < 8; ++t)
+                        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[t]) : "r"(src + t * kTileW * 4));
+                    uint32_t h[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const __half2 hv = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+                        h[i] = *reinterpret_cast<const uint32_t*>(&hv);
+                    }
+                    const uint32_t dst = dst0 + static_cast<uint32_t>(g * p.k_pad) * 16u;
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(h[0]),
+                                 "r"(h[1]), "r"(h[2]), "r"(h[3])
+                                 : "memory");
                 }
-                const uint32_t dst = bbase + static_cast<uint32_t>((g * p.k_pad + k) * 16);
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(h[0]),
-                             "r"(h[1]), "r"(h[2]), "r"(h[3])
-                             : "memory");
             }
             fence_proxy_async_smem();  // generic-proxy writes -> tensor-core reads
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(&b_full[s]);
-                mbar_arrive(&patch_empty[s]);
+                mbar_arrive(&patch_empty[ps]);
             }
         }
     } else {
@@ -244,15 +255,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t q = static_cast<uint32_t>(warp % 4);
         const int m = static_cast<int>(q * 32 + lane);
         const int dx = m / kTileH, dy = m % kTileH;
-        const int x_end = p.gx - p.r, y_end = p.y_hi;
+        const int x_end = p.gx - p.r, y_end = DIMS == 2 ? p.slow_hi : p.y_end;
+        const int64_t tile_row = static_cast<int64_t>(kTileH) * p.row_pitch;
         int it = 0;
         for (int b = blockIdx.x; b < p.nbatch; b += gridDim.x, ++it) {
             const int s = it & 1;
             const uint32_t ph = (it >> 1) & 1;
             int X0, Y0, Z0;
             batch_coords(b, X0, Y0, Z0);
-            float* out_plane = p.out + (DIMS == 3 ? static_cast<int64_t>(Z0 + p.r) * p.plane_pitch : 0) +
-                               p.left_pad;
+            // output (x, y) of D row m, tile (0, 0) of the batch
+            const int x0 = X0 + dx + p.r, y0 = Y0 + dy;  // y0: interior row
+            float* o = p.out + (DIMS == 3 ? static_cast<int64_t>(Z0 + p.r) * p.plane_pitch : 0) +
+                       static_cast<int64_t>(y0 + p.r) * p.row_pitch + p.left_pad + x0;
+            const bool full = X0 + TXB * kTileW + p.r <= x_end && Y0 + TYB * kTileH <= y_end;
             mbar_wait(&d_full[s], ph);
             tc_fence_after();
 #pragma unroll 1
@@ -260,13 +275,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t v[16];
                 tmem_ld_32x32b_x16(tmem + ((q * 32u) << 16) + static_cast<uint32_t>(s * N + c0), v);
                 tmem_wait_ld();
+                if (full) {
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int n = c0 + i;
-                    const int x = X0 + (n % TXB) * kTileW + dx + p.r;
-                    const int yi = Y0 + (n / TXB) * kTileH + dy;  // interior row
-                    if (x < x_end && yi < y_end)
-                        out_plane[static_cast<int64_t>(yi + p.r) * p.row_pitch + x] = __uint_as_float(v[i]);
+                    for (int i = 0; i < 16; ++i) {
+                        const int n = c0 + i;
+                        o[(n / TXB) * tile_row + (n % TXB) * kTileW] = __uint_as_float(v[i]);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int n = c0 + i;
+                        const bool ok = x0 + (n % TXB) * kTileW < x_end && y0 + (n / TXB) * kTileH < y_end;
+                        if (ok) o[(n / TXB) * tile_row + (n % TXB) * kTileW] = __uint_as_float(v[i]);
+                    }
                 }
             }
             tc_fence_before();

@@ -206,6 +206,18 @@ sst_status sst_compiled_plan_desc(const sst_compiled* c, sst_plan_desc* d) {
     }
 }
 
+sst_status sst_random_grid(int ndims, const uint64_t* dims, uint64_t seed, float* out) {
+    try {
+        if (!dims || !out || ndims < 1 || ndims > 3) throw std::invalid_argument("bad grid");
+        std::vector<std::size_t> d(dims, dims + ndims);
+        const stensor::Grid g = stensor::random_grid(d, seed);
+        for (std::size_t i = 0; i < g.values.size(); ++i) out[i] = static_cast<float>(g.values[i]);
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
 const char* sst_last_error(void) { return sstc::g_last_error.c_str(); }
 
 const char* sst_version(void) { return "sparstencil-b200 0.1.0 (sm_100a, tcgen05.mma.sp kind::f16)"; }

@@ -1,0 +1,229 @@
+"""Slab decomposition of a stencil sweep over the GPUs of one node.
+
+Each rank owns H consecutive slices of the slowest axis (rows in 2D, planes in
+3D) of a global grid of H*world slices and keeps r halo slices on every side
+that has a neighbour. One time step is
+
+    isend/irecv halos (NCCL, torch.distributed)   ||   interior slices [2r, n-2r)
+    wait for the halos
+    boundary slices [r, 2r) and [n-2r, n-r)
+
+so the exchange overlaps the bulk of the compute. The
+compute is the engine's sm_100a kernel restricted to a slice window
+(sst_set_row_window); the exchange is pure plumbing on views of the plan's
+ping-pong buffers. With world == 1 a step is a single full-interior launch.
+
+The index bookkeeping (which slices a rank owns, sends and receives) lives in
+`SlabLayout` so it is testable without a GPU (tests/test_multigpu.py runs it
+over gloo with world_size 2).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class SlabLayout:
+    """Slices of the slowest axis held by one rank (all in global coordinates)."""
+
+    owned: int   # H: slices owned per rank
+    world: int
+    rank: int
+    r: int       # stencil radius = halo width
+
+    @property
+    def global_slices(self) -> int:
+        return self.owned * self.world
+
+    @property
+    def lo(self) -> int:  # first global slice stored locally
+        return max(0, self.rank * self.owned - self.r)
+
+    @property
+    def hi(self) -> int:  # one past the last global slice stored locally
+        return min(self.global_slices, (self.rank + 1) * self.owned + self.r)
+
+    @property
+    def local_slices(self) -> int:
+        return self.hi - self.lo
+
+    @property
+    def has_up(self) -> bool:
+        return self.rank > 0
+
+    @property
+    def has_down(self) -> bool:
+        return self.rank + 1 < self.world
+
+    # local slice ranges [a, b)
+    def send_up(self):  # my first r owned slices -> upper neighbour's bottom halo
+        return (self.r, 2 * self.r) if self.has_up else None
+
+    def recv_up(self):  # my top halo <- upper neighbour's last r owned slices
+        return (0, self.r) if self.has_up else None
+
+    def send_down(self):
+        n = self.local_slices
+        return (n - 2 * self.r, n - self.r) if self.has_down else None
+
+    def recv_down(self):
+        n = self.local_slices
+        return (n - self.r, n) if self.has_down else None
+
+    def computed(self):
+        """Local interior window the kernel updates: [r, n - r)."""
+        return (self.r, self.local_slices - self.r)
+
+    def interior_window(self):
+        """Slices whose stencil inputs are all local before the exchange."""
+        a, b = self.computed()
+        if self.has_up:
+            a += self.r
+        if self.has_down:
+            b -= self.r
+        return (a, b)
+
+    def boundary_windows(self):
+        out = []
+        a, b = self.computed()
+        if self.has_up:
+            out.append((a, a + self.r))
+        if self.has_down:
+            out.append((b - self.r, b))
+        return out
+
+
+def exchange_halos(layout: SlabLayout, slab, pitch: int, group=None):
+    """Post the halo exchange on a flat view of the current buffer.
+
+    `slab` is a 1-D tensor over the storage buffer (elements), slice i spanning
+    [i*pitch, (i+1)*pitch). Returns the list of pending works (wait() them)."""
+    import torch.distributed as dist
+
+    ops = []
+
+    def view(rng):
+        a, b = rng
+        return slab[a * pitch:b * pitch]
+
+    if layout.has_up:
+        ops.append(dist.P2POp(dist.isend, view(layout.send_up()), layout.rank - 1, group))
+        ops.append(dist.P2POp(dist.irecv, view(layout.recv_up()), layout.rank - 1, group))
+    if layout.has_down:
+        ops.append(dist.P2POp(dist.isend, view(layout.send_down()), layout.rank + 1, group))
+        ops.append(dist.P2POp(dist.irecv, view(layout.recv_down()), layout.rank + 1, group))
+    if not ops:
+        return []
+    return dist.batch_isend_irecv(ops)
+
+
+class SlabStencil:
+    """A rank's share of a slab-decomposed stencil sweep on its B200."""
+
+    def __init__(self, stencil: str, dims_per_rank: Sequence[int], rank: int = 0, world: int = 1,
+                 device: int = 0, group=None):
+        import torch
+
+        from .engine import Compiled, SparseStencil
+
+        self.stencil = stencil
+        probe = Compiled(stencil, list(dims_per_rank))
+        r = (int(probe.info["k"]) - 1) // 2
+        probe.close()
+        self.layout = SlabLayout(owned=int(dims_per_rank[0]), world=world, rank=rank, r=r)
+        self.local_dims = [self.layout.local_slices, *[int(d) for d in dims_per_rank[1:]]]
+        self.owned_dims = list(dims_per_rank)
+        self.device = device
+        self.group = group
+        self.eng = SparseStencil(stencil, self.local_dims, device=device)
+        self.bufs = self.eng.bind_torch()
+        self.flat = [b.view(torch.float32) for b in self.bufs]
+        st = self.eng.storage
+        self.pitch = int(st["plane_pitch"] if len(self.local_dims) == 3 else st["row_pitch"])
+        self.cur = 0
+
+    # -- data --------------------------------------------------------------
+    def make_local_input(self, seed: int = 1):
+        """Synthetic dyadic input for this rank's local slices (device tensor)."""
+        import torch
+
+        from ._capi import lib
+        import ctypes as C
+
+        n = int(np.prod(self.local_dims))
+        host = np.empty(self.local_dims, dtype=np.float32)
+        dims = (C.c_uint64 * len(self.local_dims))(*self.local_dims)
+        from ._capi import check
+        check(lib().sst_random_grid(len(self.local_dims), dims, int(seed) + self.layout.rank,
+                                    host.ctypes.data_as(C.c_void_p)))
+        assert host.size == n
+        return torch.from_numpy(host).to(torch.device("cuda", self.device))
+
+    def load(self, grid):
+        self.eng.upload(grid, which=0)
+        self.cur = 0
+
+    def result(self):
+        return self.eng.download(self.cur)
+
+    # -- stepping ----------------------------------------------------------
+    def kernels_per_step(self) -> int:
+        return 1 + len(self.layout.boundary_windows())
+
+    def launches(self) -> int:
+        return int(self.eng.stats()["launches"])
+
+    def interior_cells(self) -> int:
+        r = self.layout.r
+        cells = 1
+        a, b = self.layout.computed()
+        cells *= (b - a)
+        for d in self.local_dims[1:]:
+            cells *= d - 2 * r
+        return cells
+
+    def _window(self, a: int, b: int):
+        # kernel windows are in interior coordinates of the local grid (slice - r)
+        r = self.layout.r
+        self.eng.set_row_window(a - r, b - r)
+
+    def step(self, steps: int = 1):
+        import torch
+
+        stream = torch.cuda.current_stream(torch.device("cuda", self.device)).cuda_stream
+        if self.layout.world == 1:
+            self.eng.set_row_window(0, 0)
+            self.cur = self.eng.run(steps, src=self.cur, stream=stream)
+            return
+        for _ in range(steps):
+            works = exchange_halos(self.layout, self.flat[self.cur], self.pitch, self.group)
+            a, b = self.layout.interior_window()
+            self._window(a, b)
+            self.eng.run(1, src=self.cur, stream=stream)
+            for w in works:
+                w.wait()
+            for a, b in self.layout.boundary_windows():
+                self._window(a, b)
+                self.eng.run(1, src=self.cur, stream=stream)
+            self.cur ^= 1
+        self.eng.set_row_window(0, 0)
+
+    def apply_host(self, host: np.ndarray, steps: int) -> np.ndarray:
+        """End to end from host memory through the public API."""
+        if self.layout.world == 1:
+            return self.eng.apply_host(host, steps)
+        import torch
+
+        self.eng.upload(np.ascontiguousarray(host, dtype=np.float32), which=0)
+        self.cur = 0
+        self.step(steps)
+        out = np.empty(self.local_dims, dtype=np.float32)
+        self.eng.download(self.cur, out)
+        torch.cuda.synchronize(torch.device("cuda", self.device))
+        return out
+
+    def close(self):
+        self.eng.close()
