@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -53,8 +54,8 @@ struct Variant {
     int dims, tyb, np;
     sst::SmemLayout (*layout)(int nks, int k_pad, int pw, int ph, int planes);
     void (*configure)(int smem);
-    void (*launch)(int grid, int smem, cudaStream_t st, const CUtensorMap& tm,
-                   const sst::StepParams& p);
+    void (*launch)(int grid, int smem, cudaStream_t st, const CUtensorMap& tin,
+                   const CUtensorMap& tout, const sst::StepParams& p);
 };
 
 template <int D, int TYB, int NP>
@@ -64,16 +65,16 @@ Variant make_variant() {
     v.tyb = TYB;
     v.np = NP;
     v.layout = [](int nks, int k_pad, int pw, int ph, int planes) {
-        return sst::smem_layout<8, TYB, NP>(nks, k_pad, pw, ph, planes);
+        return sst::smem_layout<TYB, NP>(nks, k_pad, pw, ph, planes);
     };
     v.configure = [](int smem) {
-        ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, 8, TYB, NP>,
+        ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
            "cudaFuncSetAttribute");
     };
-    v.launch = [](int grid, int smem, cudaStream_t st, const CUtensorMap& tm,
-                  const sst::StepParams& p) {
-        sst::stencil_step_kernel<D, 8, TYB, NP><<<grid, sst::kThreads, smem, st>>>(tm, p);
+    v.launch = [](int grid, int smem, cudaStream_t st, const CUtensorMap& tin,
+                  const CUtensorMap& tout, const sst::StepParams& p) {
+        sst::stencil_step_kernel<D, TYB, NP><<<grid, sst::kThreads, smem, st>>>(tin, tout, p);
     };
     return v;
 }
@@ -103,46 +104,81 @@ struct sst_plan {
     // device constants
     void* d_a = nullptr;
     uint32_t* d_e = nullptr;
-    int32_t* d_koff = nullptr;
-    uint8_t* d_korder = nullptr;
+    int32_t* d_gsrc = nullptr;
+    int32_t* d_gdst = nullptr;
     // ping-pong storage
     float* buf[2] = {nullptr, nullptr};
     bool owns_buf = false;
-    CUtensorMap tmap[2];
+    CUtensorMap tmap[2];      // patch loads over each buffer (whole storage)
+    CUtensorMap tmap_out[2];  // output stores, clipped to the interior (and row window)
     bool tmap_ok = false;
+    int64_t map_lo = -1, map_hi = -1;  // row window the output maps were built for
     int64_t y_lo = 0, y_hi = -1;  // interior row window
     uint64_t launches = 0;
+    int debug_mode = 0;  // SST_DEBUG_MODE (ablation experiments only)
 
     ~sst_plan() {
         cudaSetDevice(device);
         cudaFree(d_a);
         cudaFree(d_e);
-        cudaFree(d_koff);
-        cudaFree(d_korder);
+        cudaFree(d_gsrc);
+        cudaFree(d_gdst);
         if (owns_buf) {
             cudaFree(buf[0]);
             cudaFree(buf[1]);
         }
     }
 
+    static void encode(CUtensorMap* m, int rank, void* base, const cuuint64_t* dim,
+                       const cuuint64_t* stride, const cuuint32_t* box, CUtensorMapSwizzle swz) {
+        cuuint32_t estride[3] = {1, 1, 1};
+        const CUresult rc = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, static_cast<cuuint32_t>(rank),
+                                        base, dim, stride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                        swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (rc != CUDA_SUCCESS)
+            throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(rc) + ")", false);
+    }
+
+    // active interior window of the slowest axis, clamped
+    void window(int32_t& lo, int32_t& hi) const {
+        const int64_t slow = (dims == 3 ? gz : gy) - 2 * r;
+        lo = static_cast<int32_t>(y_hi > y_lo ? std::min<int64_t>(y_lo, slow) : 0);
+        hi = static_cast<int32_t>(y_hi > y_lo ? std::min<int64_t>(y_hi, slow) : slow);
+    }
+
     void make_tmaps() {
-        const int g = img.geo.patch_planes;
+        const cuuint64_t gstride[2] = {storage.row_pitch * 4, storage.plane_pitch * 4};
+        int32_t lo, hi;
+        window(lo, hi);
         for (int i = 0; i < 2; ++i) {
-            cuuint64_t gdim[3] = {storage.row_pitch, static_cast<cuuint64_t>(gy),
-                                  static_cast<cuuint64_t>(gz)};
-            cuuint64_t gstride[2] = {storage.row_pitch * 4, storage.plane_pitch * 4};
-            cuuint32_t box[3] = {static_cast<cuuint32_t>(img.geo.patch_w),
-                                 static_cast<cuuint32_t>(img.geo.patch_h), static_cast<cuuint32_t>(g)};
-            cuuint32_t estride[3] = {1, 1, 1};
-            const CUresult rc = encode_fn()(&tmap[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                                            static_cast<cuuint32_t>(dims), buf[i], gdim, gstride, box,
-                                            estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                            CU_TENSOR_MAP_SWIZZLE_NONE,
-                                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-            if (rc != CUDA_SUCCESS)
-                throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(rc) + ")", false);
+            // loads: the whole storage buffer; boxes start on 16-byte aligned columns
+            const cuuint64_t gdim[3] = {storage.row_pitch, static_cast<cuuint64_t>(gy),
+                                        static_cast<cuuint64_t>(gz)};
+            const cuuint32_t box[3] = {static_cast<cuuint32_t>(img.geo.patch_w),
+                                       static_cast<cuuint32_t>(img.geo.patch_h),
+                                       static_cast<cuuint32_t>(img.geo.patch_planes)};
+            encode(&tmap[i], dims, buf[i], gdim, gstride, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+            // stores: interior origin (16-byte aligned by the left pad), interior
+            // extents, 2D rows restricted to the active window -> TMA clips the
+            // boundary ring, ragged edges and everything outside the window
+            const int64_t row0 = r + (dims == 2 ? lo : 0);
+            const int64_t plane0 = dims == 3 ? r : 0;
+            float* base = buf[i] + plane0 * static_cast<int64_t>(storage.plane_pitch) +
+                          row0 * static_cast<int64_t>(storage.row_pitch) +
+                          static_cast<int64_t>(storage.left_pad) + r;
+            // inner extent ends on the last 16-byte boundary of the interior (TMA
+            // clips the innermost dimension in 16-byte units); the kernel writes
+            // the <= 3 remaining columns directly
+            const cuuint64_t odim[3] = {static_cast<cuuint64_t>(std::max((gx - 2 * r) & ~3, 4)),
+                                        static_cast<cuuint64_t>(dims == 2 ? std::max(hi - lo, 1) : gy - 2 * r),
+                                        static_cast<cuuint64_t>(gz - 2 * r)};
+            const cuuint32_t obox[3] = {static_cast<cuuint32_t>(sst::kBoxW),
+                                        static_cast<cuuint32_t>(tiles_y * sst::kTileH), 1u};
+            encode(&tmap_out[i], dims, base, odim, gstride, obox, CU_TENSOR_MAP_SWIZZLE_128B);
         }
+        map_lo = lo;
+        map_hi = hi;
         tmap_ok = true;
     }
 
@@ -150,9 +186,9 @@ struct sst_plan {
         sst::StepParams p{};
         p.a_img = static_cast<const uint4*>(d_a);
         p.e_words = d_e;
-        p.koff = d_koff;
-        p.korder = d_korder;
-        p.out = buf[src ^ 1];
+        p.gsrc = d_gsrc;
+        p.gdst = d_gdst;
+        p.dst = buf[src ^ 1];
         p.row_pitch = static_cast<int64_t>(storage.row_pitch);
         p.plane_pitch = static_cast<int64_t>(storage.plane_pitch);
         p.left_pad = static_cast<int32_t>(storage.left_pad);
@@ -160,9 +196,7 @@ struct sst_plan {
         p.gy = gy;
         p.gz = gz;
         p.r = r;
-        const int64_t slow = (dims == 3 ? gz : gy) - 2 * r;  // interior extent, slowest axis
-        p.slow_lo = static_cast<int32_t>(y_hi > y_lo ? std::min<int64_t>(y_lo, slow) : 0);
-        p.slow_hi = static_cast<int32_t>(y_hi > y_lo ? std::min<int64_t>(y_hi, slow) : slow);
+        window(p.slow_lo, p.slow_hi);
         p.y_end = gy - 2 * r;
         const int bw = img.geo.tiles_x * sst::kTileW, bh = tiles_y * sst::kTileH;
         p.nbx = (gx - 2 * r + bw - 1) / bw;
@@ -179,6 +213,7 @@ struct sst_plan {
         p.patch_w = img.geo.patch_w;
         p.patch_h = img.geo.patch_h;
         p.patch_planes = img.geo.patch_planes;
+        p.debug_mode = debug_mode;
         return p;
     }
 
@@ -186,7 +221,8 @@ struct sst_plan {
         const sst::StepParams p = step_params(src);
         if (p.nbatch <= 0) return;
         const int grid = std::min(p.nbatch, num_sms);
-        variant->launch(grid, smem, st, tmap[src], p);
+        if (p.slow_lo != map_lo || p.slow_hi != map_hi) make_tmaps();  // window changed
+        variant->launch(grid, smem, st, tmap[src], tmap_out[src ^ 1], p);
         ck(cudaGetLastError(), "kernel launch");
         ++launches;
     }
@@ -266,6 +302,7 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
         P->img = stensor::build_device_image(geo, d->rows, d->cols, d->a_values, d->a_meta,
                                              origin.data(), d->window_w, d->window_h);
         P->variant->configure(P->smem);
+        if (const char* dm = std::getenv("SST_DEBUG_MODE")) P->debug_mode = std::atoi(dm);
 
         P->storage.left_pad = lp;
         P->storage.row_pitch = (lp + static_cast<uint64_t>(P->gx) + 3) / 4 * 4;
@@ -278,11 +315,12 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
         ck(cudaMalloc(&P->d_e, P->img.e_words.size() * 4), "cudaMalloc");
         ck(cudaMemcpy(P->d_e, P->img.e_words.data(), P->img.e_words.size() * 4, cudaMemcpyHostToDevice),
            "cudaMemcpy");
-        ck(cudaMalloc(&P->d_koff, P->img.koff.size() * 4), "cudaMalloc");
-        ck(cudaMemcpy(P->d_koff, P->img.koff.data(), P->img.koff.size() * 4, cudaMemcpyHostToDevice),
+        ck(cudaMalloc(&P->d_gsrc, P->img.gather_src.size() * 4), "cudaMalloc");
+        ck(cudaMemcpy(P->d_gsrc, P->img.gather_src.data(), P->img.gather_src.size() * 4,
+                      cudaMemcpyHostToDevice),
            "cudaMemcpy");
-        ck(cudaMalloc(&P->d_korder, P->img.kgroup_order.size()), "cudaMalloc");
-        ck(cudaMemcpy(P->d_korder, P->img.kgroup_order.data(), P->img.kgroup_order.size(),
+        ck(cudaMalloc(&P->d_gdst, P->img.gather_dst.size() * 4), "cudaMalloc");
+        ck(cudaMemcpy(P->d_gdst, P->img.gather_dst.data(), P->img.gather_dst.size() * 4,
                       cudaMemcpyHostToDevice),
            "cudaMemcpy");
         *out = P.release();

@@ -143,6 +143,16 @@ DeviceImage build_device_image(const BatchGeometry& geo_in, std::size_t rows, st
             std::swap(img.kgroup_order[a], img.kgroup_order[b]);
     }
     schedule_cost(img.kgroup_order, img.koff, &img.worst_bank_conflict);
+
+    // ---- per-lane gather tables: sweep j, lane -> (patch byte offset, B byte offset)
+    img.gather_src.resize(k_pad / 32 * 32);
+    img.gather_dst.resize(k_pad / 32 * 32);
+    for (std::size_t j = 0; j < k_pad / 32; ++j)
+        for (std::size_t lane = 0; lane < 32; ++lane) {
+            const std::size_t k = static_cast<std::size_t>(img.kgroup_order[4 * j + lane / 8]) * 8 + lane % 8;
+            img.gather_src[j * 32 + lane] = img.koff[k] * 4;
+            img.gather_dst[j * 32 + lane] = static_cast<std::int32_t>(k) * 16;
+        }
     return img;
 }
 

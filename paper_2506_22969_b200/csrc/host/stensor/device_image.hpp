@@ -32,6 +32,9 @@ struct DeviceImage {
     std::vector<std::uint32_t> e_words;   // [k_steps][128] TMEM metadata words
     std::vector<std::int32_t> koff;       // [k_pad] patch element offset of B'' row q
     std::vector<std::uint8_t> kgroup_order;  // [k_pad/8] gather schedule (groups of 8 rows)
+    // flattened schedule, [k_pad/32][32]: lane's patch byte offset and its
+    // byte offset inside one 8-tile B'' group (MN-major: row k at k * 16 B)
+    std::vector<std::int32_t> gather_src, gather_dst;
     int worst_bank_conflict = 0;          // max lanes per bank over gather LDS sweeps
 };
 

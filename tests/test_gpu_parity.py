@@ -45,7 +45,8 @@ def run(name, grid, steps):
 
 
 @pytest.mark.parametrize("name", PRESETS_2D)
-@pytest.mark.parametrize("dims", [(97, 301), (130, 129), (64, 128), (300, 517), (21, 23)])
+@pytest.mark.parametrize("dims", [(97, 301), (130, 129), (64, 128), (300, 517), (21, 23),
+                                  (9, 9), (70, 10), (33, 134)])
 def test_one_step_bit_exact_2d(gpu, name, dims):
     g = oracle.random_grid(dims, seed=1)
     got, _ = run(name, g, 1)
