@@ -203,13 +203,13 @@ def run_engine(args, cfg, cfg_name):
     # weak scaling: each rank owns a slab of `dims` rows (plus halo rows)
     from paper_2506_22969_b200.multigpu import SlabStencil
 
-    eng = SlabStencil(stencil, dims, rank=rank, world=ws, device=local)
+    eng = SlabStencil(stencil, dims, rank=rank, world=ws, device=local, fuse=args.fuse)
     grid = eng.make_local_input(seed=1)  # dense fp32 torch tensor on the device
     eng.load(grid)
     stream = torch.cuda.current_stream(dev)
 
     for _ in range(args.warmup):
-        eng.step(1)
+        eng.step(args.fuse)
     torch.cuda.synchronize(dev)
     if ws > 1:
         dist.barrier()
@@ -238,14 +238,16 @@ def run_engine(args, cfg, cfg_name):
     cells_global = int(np.prod(dims)) * ws
     value = args.steps * cells_global / (ms / 1e3) / 1e9
 
-    # roofline of the dominant kernel: 8 B per interior update (read 4 + write 4)
+    # roofline of the dominant kernel: one launch reads the grid and writes the
+    # interior once, 8 B per interior cell (read 4 + write 4), whatever the
+    # fusion factor (a fused launch advances `fuse` time steps).
     interior = eng.interior_cells()
-    t_launch = ms / 1e3 / max(1, launches) * (launches / max(1, args.steps * eng.kernels_per_step()))
-    t_kernel = ms / 1e3 / args.steps / eng.kernels_per_step() * eng.kernels_per_step()
+    operator_steps = args.steps // args.fuse          # launches of the stencil operator
+    t_kernel = ms / 1e3 / operator_steps              # per operator application (all windows)
     alg_bytes = 8.0 * interior
     peak, peak_kind = _peaks()
     achieved = alg_bytes / t_kernel / 1e9
-    traffic = _load_traffic(cfg_name)
+    traffic = _load_traffic(cfg_name if args.fuse == 1 else f"{cfg_name}_fuse{args.fuse}")
 
     # e2e through the public API from host memory (rank-local slab)
     e2e = None
@@ -281,6 +283,7 @@ def run_engine(args, cfg, cfg_name):
         "config": {"workload": f"{stencil} {'x'.join(map(str, dims))} per GPU, "
                                f"{args.steps} time steps (one bench step = one time step)",
                    "stencil": stencil, "grid_per_gpu": list(dims), "time_steps": args.steps,
+                   "temporal_fusion": args.fuse,
                    "storage": "fp32", "operands": "f16 (tcgen05.mma.sp kind::f16), f32 accumulate",
                    "layout": "(r1, r2) = (16, 8), m' = 128",
                    "l2": "inputs larger than L2 (grid > 126 MB)" if cells_global * 4 > 126e6
@@ -311,6 +314,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--fuse", type=int, default=1,
+                    help="temporal fusion factor (reference fuse_time_steps); steps count original time steps")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.steps is None:

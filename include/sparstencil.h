@@ -104,6 +104,7 @@ typedef struct sst_plan_desc {
     const uint64_t* col_origin; /* cols entries, UINT64_MAX = zero column */
     uint64_t window_w, window_h, window_d;
     int32_t precision;        /* SST_PREC_F16 */
+    uint32_t fuse;            /* time steps per operator application (fuse_time_steps); 0 = 1 */
 } sst_plan_desc;
 
 /* Pointers into the compiled object; valid while `c` lives. */
@@ -144,7 +145,9 @@ SST_API sst_status sst_plan_bind(sst_plan* plan, void* buf0, void* buf1);
 SST_API sst_status sst_upload(sst_plan* plan, int which, const float* src, int src_on_device,
                       void* stream);
 SST_API sst_status sst_download(sst_plan* plan, int which, float* dst, int dst_on_device, void* stream);
-/* Run `steps` time steps starting from buffer `src`; *dst_out receives the
+/* Run `steps` time steps (original, unfused steps: a plan compiled with fuse f
+ * launches steps / f times and needs steps % f == 0) starting from buffer
+ * `src`; *dst_out receives the
  * buffer holding the result. The interior [r, N-r) of every axis is updated
  * each step; the boundary ring keeps the input values, so after T steps the
  * core [T*r, N-T*r) equals the reference's valid-region sweep. */

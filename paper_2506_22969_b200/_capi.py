@@ -69,7 +69,7 @@ class PlanDesc(C.Structure):
                 ("a_values", C.POINTER(C.c_double)), ("a_meta", C.POINTER(C.c_uint8)),
                 ("col_origin", C.POINTER(C.c_uint64)),
                 ("window_w", C.c_uint64), ("window_h", C.c_uint64), ("window_d", C.c_uint64),
-                ("precision", C.c_int32)]
+                ("precision", C.c_int32), ("fuse", C.c_uint32)]
 
 
 class Storage(C.Structure):

@@ -116,6 +116,7 @@ struct sst_plan {
     int64_t y_lo = 0, y_hi = -1;  // interior row window
     uint64_t launches = 0;
     int debug_mode = 0;  // SST_DEBUG_MODE (ablation experiments only)
+    uint64_t fuse = 1;   // original time steps per launch
 
     ~sst_plan() {
         cudaSetDevice(device);
@@ -255,6 +256,7 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
         P->dims = d->dims;
         P->k = d->k;
         P->r = (d->k - 1) / 2;
+        P->fuse = d->fuse > 1 ? d->fuse : 1;
         P->gx = static_cast<int>(d->grid_dims[d->dims - 1]);
         P->gy = static_cast<int>(d->grid_dims[d->dims - 2]);
         P->gz = d->dims == 3 ? static_cast<int>(d->grid_dims[0]) : 1;
@@ -462,8 +464,10 @@ sst_status sst_run_steps(sst_plan* plan, int src, uint64_t steps, void* stream, 
         if (!plan->tmap_ok) throw std::invalid_argument("plan has no bound buffers");
         ck(cudaSetDevice(plan->device), "cudaSetDevice");
         const auto st = static_cast<cudaStream_t>(stream);
+        if (steps % plan->fuse != 0)
+            throw std::invalid_argument("steps must be a multiple of the fusion factor");
         int cur = src;
-        for (uint64_t t = 0; t < steps; ++t) {
+        for (uint64_t t = 0; t < steps / plan->fuse; ++t) {
             plan->launch(cur, st);
             cur ^= 1;
         }
@@ -483,12 +487,14 @@ sst_status sst_apply_host(sst_plan* plan, const float* h_in, float* h_out, uint6
         }
         ck(cudaSetDevice(plan->device), "cudaSetDevice");
         cudaStream_t st = nullptr;
+        if (steps % plan->fuse != 0)
+            throw std::invalid_argument("steps must be a multiple of the fusion factor");
         copy_dense(plan, 0, h_in, nullptr, true, false, st);
         // identical boundary ring in both buffers (device-side copy)
         ck(cudaMemcpyAsync(plan->buf[1], plan->buf[0], plan->storage.bytes, cudaMemcpyDeviceToDevice, st),
            "cudaMemcpyAsync(ring)");
         int cur = 0;
-        for (uint64_t t = 0; t < steps; ++t) {
+        for (uint64_t t = 0; t < steps / plan->fuse; ++t) {
             plan->launch(cur, st);
             cur ^= 1;
         }

@@ -20,6 +20,7 @@ struct sst_compiled {
     stensor::Conversion cv;
     stensor::Sparse24Matrix a2;
     std::vector<std::uint64_t> col_origin_u64;
+    std::uint64_t fuse = 1;
 };
 
 namespace sstc {
@@ -85,6 +86,7 @@ sst_status sst_compile(const char* stencil, const uint64_t* grid_dims, int ndims
         auto c = std::make_unique<sst_compiled>();
         c->spec = resolve_stencil(stencil);
         if (fuse > 1) c->spec = stensor::fuse_time_steps(c->spec, fuse);
+        c->fuse = fuse > 1 ? fuse : 1;
         if (ndims != c->spec.dims || !grid_dims)
             throw std::invalid_argument("grid dimensionality does not match stencil");
         c->dims.assign(grid_dims, grid_dims + ndims);
@@ -200,6 +202,7 @@ sst_status sst_compiled_plan_desc(const sst_compiled* c, sst_plan_desc* d) {
         d->window_h = L.stair.block_count;
         d->window_d = L.z_factor;
         d->precision = SST_PREC_F16;
+        d->fuse = static_cast<uint32_t>(c->fuse);
         return SST_OK;
     } catch (...) {
         return sstc::from_current_exception();

@@ -95,8 +95,9 @@ class SparseStencil:
         self.compiled = stencil if isinstance(stencil, Compiled) else Compiled(
             stencil, grid_dims, r1, r2, fuse)
         self.grid_dims = self.compiled.grid_dims
-        self.k = int(self.compiled.info["k"])
-        self.r = (self.k - 1) // 2
+        self.fuse = max(1, int(fuse)) if not isinstance(stencil, Compiled) else 1
+        self.k = int(self.compiled.info["k"])       # of the (possibly fused) operator
+        self.r = (self.k - 1) // 2 // self.fuse     # radius of one original time step
         desc = self.compiled.plan_desc()
         h = C.c_void_p()
         check(lib().sst_plan_create(C.byref(desc), int(device), C.byref(h)))
@@ -194,16 +195,21 @@ def valid_core(full: np.ndarray, steps: int, r: int) -> np.ndarray:
     return full[sl]
 
 
-def sparse_apply(stencil: str, grid: np.ndarray, steps: int, device: int = 0) -> np.ndarray:
+def sparse_apply(stencil: str, grid: np.ndarray, steps: int, device: int = 0,
+                 fuse: int = 1) -> np.ndarray:
     """Drop-in for stensor::direct_apply (stencil.hpp:72): valid-region result
-    (extent N - steps*(k-1) per axis) computed on the B200."""
+    (extent N - steps*(k-1) per axis) computed on the B200. `fuse` > 1 applies
+    the reference's temporal fusion (fuse_time_steps, stencil.cpp:272-347): one
+    launch advances `fuse` time steps (used when it divides `steps`)."""
     if steps < 1:
         raise _capi.InvalidArgument("steps must be >= 1")
     g = np.asarray(grid)
-    eng = SparseStencil(stencil, list(g.shape), device=device)
+    f = fuse if fuse > 1 and steps % fuse == 0 else 1
+    eng = SparseStencil(stencil, list(g.shape), device=device, fuse=f)
     try:
+        k1 = 2 * eng.r + 1
         for n in g.shape:
-            if n < eng.k + (steps - 1) * (eng.k - 1):
+            if n < k1 + (steps - 1) * (k1 - 1):
                 raise _capi.InvalidArgument("grid smaller than kernel")
         full = eng.apply_host(g.astype(np.float32), steps)
         return valid_core(full, steps, eng.r).astype(np.float64)

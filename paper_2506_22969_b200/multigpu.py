@@ -124,21 +124,22 @@ class SlabStencil:
     """A rank's share of a slab-decomposed stencil sweep on its B200."""
 
     def __init__(self, stencil: str, dims_per_rank: Sequence[int], rank: int = 0, world: int = 1,
-                 device: int = 0, group=None):
+                 device: int = 0, group=None, fuse: int = 1):
         import torch
 
         from .engine import Compiled, SparseStencil
 
         self.stencil = stencil
-        probe = Compiled(stencil, list(dims_per_rank))
-        r = (int(probe.info["k"]) - 1) // 2
+        self.fuse = max(1, int(fuse))
+        probe = Compiled(stencil, list(dims_per_rank), 16, 8, self.fuse)
+        r = (int(probe.info["k"]) - 1) // 2  # halo width of one (fused) launch
         probe.close()
         self.layout = SlabLayout(owned=int(dims_per_rank[0]), world=world, rank=rank, r=r)
         self.local_dims = [self.layout.local_slices, *[int(d) for d in dims_per_rank[1:]]]
         self.owned_dims = list(dims_per_rank)
         self.device = device
         self.group = group
-        self.eng = SparseStencil(stencil, self.local_dims, device=device)
+        self.eng = SparseStencil(stencil, self.local_dims, device=device, fuse=self.fuse)
         self.bufs = self.eng.bind_torch()
         self.flat = [b.view(torch.float32) for b in self.bufs]
         st = self.eng.storage
@@ -198,16 +199,18 @@ class SlabStencil:
             self.eng.set_row_window(0, 0)
             self.cur = self.eng.run(steps, src=self.cur, stream=stream)
             return
-        for _ in range(steps):
+        if steps % self.fuse:
+            raise ValueError("steps must be a multiple of the fusion factor")
+        for _ in range(steps // self.fuse):
             works = exchange_halos(self.layout, self.flat[self.cur], self.pitch, self.group)
             a, b = self.layout.interior_window()
             self._window(a, b)
-            self.eng.run(1, src=self.cur, stream=stream)
+            self.eng.run(self.fuse, src=self.cur, stream=stream)
             for w in works:
                 w.wait()
             for a, b in self.layout.boundary_windows():
                 self._window(a, b)
-                self.eng.run(1, src=self.cur, stream=stream)
+                self.eng.run(self.fuse, src=self.cur, stream=stream)
             self.cur ^= 1
         self.eng.set_row_window(0, 0)
 

@@ -186,3 +186,26 @@ def test_full_size_multi_step_windows(gpu):
         want = oracle.direct_apply(name, sub, steps)
         got = full[y0:y0 + 192, x0:x0 + 192].astype(np.float64)
         assert np.abs(got - want).max() <= tol_abs(steps)
+
+
+@pytest.mark.parametrize("name,fuse", [("Box-2D9P", 2), ("Heat-2D", 3), ("Box-2D9P", 4)])
+def test_temporal_fusion(gpu, name, fuse):
+    """fuse_time_steps (stencil.cpp:272-347) on the device: the fused operator's
+    dyadic weights are exact in f16, so one fused launch on dyadic data equals
+    `fuse` reference steps exactly; longer runs stay within the f16 tolerance."""
+    dims = (140, 300)
+    g = oracle.random_grid(dims, 12)
+    eng = SparseStencil(name, list(dims), fuse=fuse)
+    one = valid_core(eng.apply_host(g.astype(np.float32), fuse), fuse, eng.r).astype(np.float64)
+    assert eng.stats()["launches"] == 1
+    assert np.array_equal(one, oracle.direct_apply(name, g, fuse))
+    t = 6 * fuse
+    many = valid_core(eng.apply_host(g.astype(np.float32), t), t, eng.r).astype(np.float64)
+    from paper_2506_22969_b200 import InvalidArgument
+    with pytest.raises(InvalidArgument):
+        eng.apply_host(g.astype(np.float32), fuse + 1)
+    eng.close()
+    want = oracle.direct_apply(name, g, t)
+    assert np.abs(many - want).max() <= tol_abs(t)
+    out = sparse_apply(name, g, t, fuse=fuse)
+    assert np.array_equal(out, many)
