@@ -14,6 +14,7 @@
 
 #include "../host/capi_internal.hpp"
 #include "sparstencil.h"
+#include "stencil3d_kernel.cuh"
 #include "stencil_kernel.cuh"
 #include "stensor/device_image.hpp"
 #include "stensor/morph.hpp"
@@ -52,6 +53,7 @@ EncodeTiledFn encode_fn() {
 // patch pipeline depth). Plans pick the deepest variant that fits in smem.
 struct Variant {
     int dims, tyb, np;
+    int kz;  // 0: whole-window kernel; > 0: 3D z-streaming kernel with kz z slices
     sst::SmemLayout (*layout)(int nks, int k_pad, int pw, int ph, int planes);
     void (*configure)(int smem);
     void (*launch)(int grid, int smem, cudaStream_t st, const CUtensorMap& tin,
@@ -79,11 +81,35 @@ Variant make_variant() {
     return v;
 }
 
-// preference order per dimensionality: deepest TMA pipeline first
+template <int TYB, int NP, int KZ>
+Variant make_stream_variant() {
+    Variant v{};
+    v.dims = 3;
+    v.tyb = TYB;
+    v.np = NP;
+    v.kz = KZ;
+    v.layout = [](int nks, int k_pad, int pw, int ph, int) {
+        return sst::smem_layout_stream<TYB, NP, KZ>(nks, k_pad, pw, ph);
+    };
+    v.configure = [](int smem) {
+        ck(cudaFuncSetAttribute(sst::stencil3d_stream_kernel<TYB, NP, KZ>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+           "cudaFuncSetAttribute");
+    };
+    v.launch = [](int grid, int smem, cudaStream_t st, const CUtensorMap& tin,
+                  const CUtensorMap& tout, const sst::StepParams& p) {
+        sst::stencil3d_stream_kernel<TYB, NP, KZ><<<grid, sst::kThreads, smem, st>>>(tin, tout, p);
+    };
+    return v;
+}
+
+// preference order per dimensionality: 3D z-streaming first, then the deepest
+// TMA pipeline that fits (SST_VARIANT=<index> forces one, for experiments)
 const Variant* variants(int& n) {
     static const Variant v[] = {
         make_variant<2, 8, 4>(), make_variant<2, 8, 3>(), make_variant<2, 4, 4>(),
         make_variant<2, 8, 2>(), make_variant<2, 4, 2>(),
+        make_stream_variant<8, 2, 3>(), make_stream_variant<4, 6, 3>(), make_stream_variant<4, 4, 3>(),
         make_variant<3, 2, 4>(), make_variant<3, 2, 3>(), make_variant<3, 2, 2>(),
     };
     n = static_cast<int>(sizeof(v) / sizeof(v[0]));
@@ -210,7 +236,7 @@ struct sst_plan {
         }
         p.nbatch = p.nbx * p.nby * p.nbz;
         p.k_pad = img.geo.k_pad;
-        p.nks = img.geo.k_pad / 32;
+        p.nks = static_cast<int32_t>(img.a_smem.size() * 2 / 4096);  // K steps of the A'' image
         p.patch_w = img.geo.patch_w;
         p.patch_h = img.geo.patch_h;
         p.patch_planes = img.geo.patch_planes;
@@ -221,7 +247,9 @@ struct sst_plan {
     void launch(int src, cudaStream_t st) {
         const sst::StepParams p = step_params(src);
         if (p.nbatch <= 0) return;
-        const int grid = std::min(p.nbatch, num_sms);
+        // streaming kernels split (column, output plane) units; others stride batches
+        const int64_t work = variant->kz > 0 ? static_cast<int64_t>(p.nbx) * p.nby * p.nbz : p.nbatch;
+        const int grid = static_cast<int>(std::min<int64_t>(work, num_sms));
         if (p.slow_lo != map_lo || p.slow_hi != map_hi) make_tmaps();  // window changed
         variant->launch(grid, smem, st, tmap[src], tmap_out[src ^ 1], p);
         ck(cudaGetLastError(), "kernel launch");
@@ -281,26 +309,57 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
         geo.x_shift = static_cast<int>(lp);
         geo.patch_w = static_cast<int>(sst::align_up(
             static_cast<uint32_t>(lp + d->window_w + sst::kTileW * (geo.tiles_x - 1)), 4));
-        int nvar = 0;
-        const Variant* vars = variants(nvar);
-        for (int i = 0; i < nvar && !P->variant; ++i) {
-            if (vars[i].dims != d->dims) continue;
-            const int ph = static_cast<int>(d->window_h) + sst::kTileH * (vars[i].tyb - 1);
-            const sst::SmemLayout L = vars[i].layout(k_pad / 32, k_pad, geo.patch_w, ph, geo.patch_planes);
-            const int need = static_cast<int>(L.total) + 1024;  // slack for the 1 KiB base alignment
-            if (need > max_smem || ph > 256) continue;
-            P->variant = &vars[i];
-            P->smem = need;
-            geo.tiles_y = vars[i].tyb;
-            geo.patch_h = ph;
-        }
-        if (!P->variant)
-            throw std::invalid_argument("stencil too wide for one CTA's shared memory");
-        P->tiles_y = geo.tiles_y;
         std::vector<std::size_t> origin(d->cols);
         for (std::size_t i = 0; i < d->cols; ++i)
             origin[i] = d->col_origin[i] == UINT64_MAX ? stensor::npos
                                                        : static_cast<std::size_t>(d->col_origin[i]);
+        // 3D z-streaming needs A'' to split into kz 4-group-aligned z slices with
+        // identical (u, v) order (true for expand_units layouts); probe it
+        const int kz = d->dims == 3 ? static_cast<int>(d->window_d) : 0;
+        bool can_stream = false;
+        int k_pad_z = 0;
+        if (kz > 1 && d->cols % static_cast<uint64_t>(kz) == 0) {
+            try {
+                stensor::BatchGeometry g2 = geo;
+                g2.z_slices = kz;
+                g2.patch_planes = 1;
+                g2.patch_h = static_cast<int>(d->window_h);
+                const auto probe = stensor::build_device_image(g2, d->rows, d->cols, d->a_values,
+                                                               d->a_meta, origin.data(), d->window_w,
+                                                               d->window_h);
+                k_pad_z = probe.geo.k_pad;
+                can_stream = true;
+            } catch (const std::invalid_argument&) {
+                can_stream = false;
+            }
+        }
+        int nvar = 0;
+        const Variant* vars = variants(nvar);
+        const char* force = std::getenv("SST_VARIANT");
+        const int forced = force ? std::atoi(force) : -1;
+        for (int i = 0; i < nvar && !P->variant; ++i) {
+            const Variant& v = vars[i];
+            if (v.dims != d->dims || (forced >= 0 && i != forced)) continue;
+            if (v.kz > 0 && (!can_stream || v.kz != kz)) continue;
+            const int ph = static_cast<int>(d->window_h) + sst::kTileH * (v.tyb - 1);
+            const int kp = v.kz > 0 ? k_pad_z : k_pad;
+            const int nks = v.kz > 0 ? kz * k_pad_z / 32 : k_pad / 32;
+            const int planes = v.kz > 0 ? 1 : geo.patch_planes;
+            const sst::SmemLayout L = v.layout(nks, kp, geo.patch_w, ph, planes);
+            const int need = static_cast<int>(L.total) + 1024;  // slack for the 1 KiB base alignment
+            if (need > max_smem || ph > 256) continue;
+            P->variant = &v;
+            P->smem = need;
+            geo.tiles_y = v.tyb;
+            geo.patch_h = ph;
+            if (v.kz > 0) {
+                geo.z_slices = kz;
+                geo.patch_planes = 1;
+            }
+        }
+        if (!P->variant)
+            throw std::invalid_argument("stencil too wide for one CTA's shared memory");
+        P->tiles_y = geo.tiles_y;
         P->img = stensor::build_device_image(geo, d->rows, d->cols, d->a_values, d->a_meta,
                                              origin.data(), d->window_w, d->window_h);
         P->variant->configure(P->smem);

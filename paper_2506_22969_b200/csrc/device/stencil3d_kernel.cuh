@@ -1,0 +1,239 @@
+// stencil3d_kernel.cuh — z-streaming variant of the step kernel for 3D stencils.
+//
+// A 3D stencil's A'' is z-major (expand_units, convert.cpp:376-396): KZ slices of
+// C columns, slice dz holding the weights of input plane z = dz of the window.
+// The output plane zo is therefore sum_dz A_dz * B(zo + dz), where B(z) is the
+// 2D-window gather of ONE input plane. Instead of gathering a kz-plane window per
+// output plane (kz times the gather and smem traffic), a CTA walks a run of
+// output planes of one (x, y) column and, per input plane z:
+//
+//   TMA    one plane patch (ring of NP)           warp 0
+//   gather B(z) once (K = C rounded to 32)        warps 2-5
+//   MMA    D(z - dz) += A_dz * B(z), dz = 0..KZ-1  warp 1 (accumulators live in a
+//          TMEM ring of NACC = KZ + 1 slots; D(z - KZ + 1) completes each plane)
+//   store  completed D planes                      warps 6-9
+//
+// Work split: output units (column, zo) in column-major order are cut into one
+// contiguous range per CTA (perfect balance); a range re-enters the pipeline
+// (2r extra planes) only where it starts a new column.
+#pragma once
+
+#include "stencil_kernel.cuh"
+
+namespace sst {
+
+template <int TYB, int NP, int KZ>
+__host__ __device__ inline SmemLayout smem_layout_stream(int nks, int k_pad, int patch_w, int patch_h) {
+    constexpr int NACC = KZ + 1;
+    return smem_layout_generic<TYB>(nks, k_pad, patch_w, patch_h, 1, NP, 2, 2 * NP + 4 + 2 * NACC);
+}
+
+// Iterates the runs of a CTA's unit range: calls fn(col, zo_a, zo_b) for each run
+// (window-relative output planes, inclusive).
+template <class Fn>
+__device__ __forceinline__ void for_each_run(int u0, int u1, int ozw, Fn&& fn) {
+    for (int u = u0; u < u1;) {
+        const int col = u / ozw, zo_a = u % ozw;
+        const int len = min(u1 - u, ozw - zo_a);
+        fn(col, zo_a, zo_a + len - 1);
+        u += len;
+    }
+}
+
+template <int TYB, int NP, int KZ>
+__global__ void __launch_bounds__(kThreads, 1)
+    stencil3d_stream_kernel(const __grid_constant__ CUtensorMap tmap_in,
+                            const __grid_constant__ CUtensorMap tmap_out, const StepParams p) {
+    constexpr int N = kTXB * TYB;
+    constexpr int CW = 2 * TYB;
+    constexpr int NBOX = kTXB / 2;
+    constexpr int NGROUP = N / 8;
+    constexpr int GPW = NGROUP >= kGatherWarps ? NGROUP / kGatherWarps : 1;
+    constexpr int NACC = KZ + 1;
+    constexpr int R = (KZ - 1) / 2;
+    static_assert(N % 16 == 0 && N <= 128, "UMMA N for M=128");
+    static_assert(NACC * N <= 256, "accumulator ring must leave TMEM room for metadata");
+    using namespace ptx;
+
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const SmemLayout L = smem_layout_stream<TYB, NP, KZ>(p.nks, p.k_pad, p.patch_w, p.patch_h);
+    uint8_t* sA = smem + L.a;
+    uint8_t* sB = smem + L.b;
+    uint8_t* sS = smem + L.s;
+    uint8_t* sP = smem + L.p;
+    int32_t* sGsrc = reinterpret_cast<int32_t*>(smem + L.gsrc);
+    int32_t* sGdst = reinterpret_cast<int32_t*>(smem + L.gdst);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
+    uint64_t* patch_full = bars;
+    uint64_t* patch_empty = bars + NP;
+    uint64_t* b_full = bars + 2 * NP;
+    uint64_t* b_empty = b_full + 2;
+    uint64_t* d_full = b_full + 4;
+    uint64_t* d_empty = d_full + NACC;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem_slot);
+
+    const int warp = threadIdx.x / 32;
+    const uint32_t lane = lane_id();
+    const int ksz = p.k_pad / 32;  // K steps per z slice
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NP; ++s) {
+            mbar_init(&patch_full[s], 1);
+            mbar_init(&patch_empty[s], kGatherWarps);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&b_full[s], kGatherWarps);
+            mbar_init(&b_empty[s], 1);
+        }
+        for (int s = 0; s < NACC; ++s) {
+            mbar_init(&d_full[s], 1);
+            mbar_init(&d_empty[s], kEpiWarps);
+        }
+        fence_mbar_init();
+        tma_prefetch_desc(&tmap_in);
+        tma_prefetch_desc(&tmap_out);
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    stage_constants(p, sA, sGsrc, sGdst);
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t e_col = NACC * N;  // metadata after the accumulator ring
+    if (warp >= kEpiWarp0) store_metadata(p, tmem, e_col, static_cast<uint32_t>(warp % 4), lane);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    // this CTA's contiguous range of (column, output plane) units
+    const int ozw = p.slow_hi - p.slow_lo;
+    const int64_t units = static_cast<int64_t>(p.nbx) * p.nby * ozw;
+    const int u0 = static_cast<int>(units * blockIdx.x / gridDim.x);
+    const int u1 = static_cast<int>(units * (blockIdx.x + 1) / gridDim.x);
+    auto col_xy = [&](int col, int& X0, int& Y0) {
+        X0 = (col % p.nbx) * (kTXB * kTileW);
+        Y0 = (col / p.nbx) * (TYB * kTileH);
+    };
+
+    if (warp == 0) {
+        // ------------------------------------------------------ TMA producer
+        if (elect_one()) {
+            const uint32_t pbytes = static_cast<uint32_t>(p.patch_w * p.patch_h) * 4u;
+            int it = 0;
+            for_each_run(u0, u1, ozw, [&](int col, int zo_a, int zo_b) {
+                int X0, Y0;
+                col_xy(col, X0, Y0);
+                // input (storage) planes of outputs zo_a..zo_b: zo_a .. zo_b + 2R
+                for (int z = p.slow_lo + zo_a; z <= p.slow_lo + zo_b + 2 * R; ++z, ++it) {
+                    const int s = it % NP;
+                    mbar_wait(&patch_empty[s], ((it / NP) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&patch_full[s], pbytes);
+                    tma_load_3d(sP + s * L.p_stride, &tmap_in, &patch_full[s], X0, Y0, z);
+                }
+            });
+        }
+    } else if (warp == 1) {
+        // -------------------------------------------------------- MMA issuer
+        const uint32_t idesc = make_idesc_f16(128, N, true, 0, 1);
+        const uint32_t b_sbo = static_cast<uint32_t>(p.k_pad) * 16u;
+        const uint32_t a0 = smem_u32(sA);
+        int it = 0, obase = 0;
+        for_each_run(u0, u1, ozw, [&](int col, int zo_a, int zo_b) {
+            (void)col;
+            for (int zi = zo_a; zi <= zo_b + 2 * R; ++zi, ++it) {  // window-relative input plane
+                const int s = it & 1;
+                mbar_wait(&b_full[s], (it >> 1) & 1);
+                // a new accumulator starts at dz = 0 (zo = zi): wait until it is drained
+                if (zi <= zo_b) {
+                    const int o = obase + (zi - zo_a);
+                    mbar_wait(&d_empty[o % NACC], ((o / NACC) & 1) ^ 1);
+                }
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t b0 = smem_u32(sB + s * L.b_stride);
+#pragma unroll
+                    for (int dz = 0; dz < KZ; ++dz) {
+                        const int zo = zi - dz;
+                        if (zo < zo_a || zo > zo_b) continue;
+                        const int slot = (obase + (zo - zo_a)) % NACC;
+                        for (int ks = 0; ks < ksz; ++ks) {
+                            const int kk = dz * ksz + ks;  // A'' / metadata K step
+                            const uint64_t ad = make_smem_desc(a0 + kk * 4096u, 128, 256);
+                            const uint64_t bd = make_smem_desc(b0 + ks * 512u, 128, b_sbo);
+                            const uint32_t ea = tmem + e_col + static_cast<uint32_t>(kk);
+                            mma_sp_f16(tmem + static_cast<uint32_t>(slot * N), ad, bd, ea & ~1u,
+                                       idesc | (ea & 1u), (dz > 0 || ks > 0) ? 1u : 0u);
+                        }
+                    }
+                    mma_commit(&b_empty[s]);
+                    const int zdone = zi - 2 * R;  // its last contribution was just issued
+                    if (zdone >= zo_a && zdone <= zo_b) mma_commit(&d_full[(obase + zdone - zo_a) % NACC]);
+                }
+                __syncwarp();
+            }
+            obase += zo_b - zo_a + 1;
+        });
+    } else if (warp < kGatherWarp0 + kGatherWarps) {
+        // ------------------------------------------------------------ gather
+        const int gw = warp - kGatherWarp0;
+        const bool active = gw < NGROUP;
+        int32_t toff[GPW][8];
+        tile_offsets<TYB, GPW>(gw, p.patch_w, toff);
+        const uint32_t gstride = static_cast<uint32_t>(p.k_pad) * 16u;
+        const int nsweeps = active ? ksz : 0;
+        int it = 0;
+        for_each_run(u0, u1, ozw, [&](int col, int zo_a, int zo_b) {
+            (void)col;
+            for (int zi = zo_a; zi <= zo_b + 2 * R; ++zi, ++it) {
+                const int ps = it % NP, s = it & 1;
+                mbar_wait(&patch_full[ps], (it / NP) & 1);
+                mbar_wait(&b_empty[s], ((it >> 1) & 1) ^ 1);
+                gather_batch<GPW>(smem_u32(sP + ps * L.p_stride), smem_u32(sB + s * L.b_stride),
+                                  sGsrc, sGdst, nsweeps, gw, gstride, lane, toff);
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&b_full[s]);
+                    mbar_arrive(&patch_empty[ps]);
+                }
+            }
+        });
+    } else {
+        // ---------------------------------------------------------- epilogue
+        const uint32_t q = static_cast<uint32_t>(warp % 4);
+        const int etid = threadIdx.x - kEpiWarp0 * 32;
+        int o = 0, nbox = 0;
+        for_each_run(u0, u1, ozw, [&](int col, int zo_a, int zo_b) {
+            int X0, Y0;
+            col_xy(col, X0, Y0);
+            for (int zo = zo_a; zo <= zo_b; ++zo, ++o) {
+                const int slot = o % NACC;
+                mbar_wait(&d_full[slot], (o / NACC) & 1);
+                tc_fence_after();
+#pragma unroll 1
+                for (int c = 0; c < NBOX; ++c, ++nbox) {
+                    uint32_t v[CW];
+                    tmem_load_box<CW>(tmem + ((q * 32u) << 16) + static_cast<uint32_t>(slot * N + c * CW), v);
+                    if (c == NBOX - 1) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&d_empty[slot]);
+                    }
+                    store_box<3, TYB>(p, &tmap_out, v, sS, L.s_stride, nbox, X0, Y0, p.slow_lo + zo, c,
+                                      q, lane, etid);
+                }
+            }
+        });
+        if (etid == 0) bulk_wait<0>();
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+}  // namespace sst

@@ -1,0 +1,178 @@
+// stencil_common.cuh — pieces shared by the sm_100a stencil kernels:
+// launch parameters, constant-operand staging, the B'' gather, and the
+// TMEM -> swizzled smem -> TMA-store epilogue of one 32-wide output box.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cstdint>
+
+#include "sm100_ptx.cuh"
+
+namespace sst {
+
+constexpr int kThreads = 320;
+constexpr int kGatherWarp0 = 2, kGatherWarps = 4;
+constexpr int kEpiWarp0 = 6, kEpiWarps = 4;
+constexpr int kTileW = 16, kTileH = 8;  // r1, r2
+constexpr int kTXB = 8;                 // tiles per batch along x (128 outputs)
+constexpr int kBoxW = 32;               // output box width (128 B, SWIZZLE_128B)
+constexpr uint32_t kEpiBarrier = 1;     // named barrier of the 4 epilogue warps
+
+struct StepParams {
+    const uint4* a_img;        // A'' smem image (fp16), nks * 4096 bytes
+    const uint32_t* e_words;   // [nks][128]
+    const int32_t* gsrc;       // [k_pad/32][32] patch byte offset of the lane's B'' row
+    const int32_t* gdst;       // [k_pad/32][32] byte offset of that row in an 8-tile group
+    float* dst;                // output storage buffer (right-edge columns, see epilogue)
+    int64_t row_pitch, plane_pitch;  // storage pitches (elements)
+    int32_t left_pad;
+    int32_t gx, gy, gz;        // logical extents
+    int32_t r;                 // radius
+    int32_t slow_lo, slow_hi;  // window over the slowest axis (y in 2D, z in 3D), interior coords
+    int32_t y_end;             // interior rows (gy - 2r)
+    int32_t nbx, nby, nbz, nbatch;
+    int32_t k_pad;             // B'' rows per MMA pass (per z slice when streaming)
+    int32_t nks;               // 32-wide K steps in the A'' image (all slices)
+    int32_t patch_w, patch_h, patch_planes;
+    int32_t debug_mode;        // ablation bits (profiling only): 1 no stores, 2 no gather, 4 no MMA
+};
+
+// tile (column n of the MMA) -> (tx, ty) of the batch: output box c (32 x-cells,
+// tiles tx = 2c, 2c+1) owns columns [c*2*TYB, (c+1)*2*TYB), n = c*2*TYB + 2*ty + (tx & 1)
+template <int TYB>
+__host__ __device__ inline void tile_of_column(int n, int& tx, int& ty) {
+    const int c = n / (2 * TYB), m = n % (2 * TYB);
+    ty = m / 2;
+    tx = 2 * c + (m & 1);
+}
+
+// A'' image and the gather tables: global -> smem (all threads)
+__device__ __forceinline__ void stage_constants(const StepParams& p, uint8_t* sA, int32_t* sGsrc,
+                                                int32_t* sGdst) {
+    const int n16 = p.nks * 4096 / 16;
+    uint4* dstA = reinterpret_cast<uint4*>(sA);
+    for (int i = threadIdx.x; i < n16; i += kThreads) dstA[i] = p.a_img[i];
+    for (int i = threadIdx.x; i < p.k_pad; i += kThreads) {  // k_pad/32 sweeps x 32 lanes
+        sGsrc[i] = p.gsrc[i];
+        sGdst[i] = p.gdst[i];
+    }
+}
+
+// 2:4 metadata -> TMEM columns [e_col, e_col + nks) (each epilogue warp its lane quarter)
+__device__ __forceinline__ void store_metadata(const StepParams& p, uint32_t tmem, uint32_t e_col,
+                                               uint32_t q, uint32_t lane) {
+    for (int ks = 0; ks < p.nks; ++ks)
+        ptx::tmem_st_32x32b_x1(tmem + ((q * 32u) << 16) + e_col + ks,
+                               p.e_words[ks * 128 + q * 32 + lane]);
+    ptx::tmem_wait_st();
+}
+
+// Patch byte offsets of the 8 tile origins of each 8-tile group a gather warp owns.
+template <int TYB, int GPW>
+__device__ __forceinline__ void tile_offsets(int gw, int patch_w, int32_t (&toff)[GPW][8]) {
+#pragma unroll
+    for (int gi = 0; gi < GPW; ++gi)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            int tx, ty;
+            tile_of_column<TYB>((gw + kGatherWarps * gi) * 8 + t, tx, ty);
+            toff[gi][t] = (ty * kTileH * patch_w + tx * kTileW) * 4;
+        }
+}
+
+// One batch of B'': B''[q, tile] = patch[tile_origin + koff[q]] as f16 (RNE), written
+// into the UMMA MN-major operand (8 tiles per 16-byte core-matrix row).
+template <int GPW>
+__device__ __forceinline__ void gather_batch(uint32_t pbase, uint32_t bbase, const int32_t* sGsrc,
+                                             const int32_t* sGdst, int nsweeps, int gw,
+                                             uint32_t gstride, uint32_t lane,
+                                             const int32_t (&toff)[GPW][8]) {
+#pragma unroll 1
+    for (int j = 0; j < nsweeps; ++j) {
+        const uint32_t src = pbase + static_cast<uint32_t>(sGsrc[j * 32 + lane]);
+        const uint32_t dst = bbase + static_cast<uint32_t>(sGdst[j * 32 + lane]);
+#pragma unroll
+        for (int gi = 0; gi < GPW; ++gi) {
+            float v[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[t]) : "r"(src + toff[gi][t]));
+            uint32_t h[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const __half2 hv = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+                h[i] = *reinterpret_cast<const uint32_t*>(&hv);
+            }
+            const uint32_t d = dst + static_cast<uint32_t>(gw + kGatherWarps * gi) * gstride;
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(d), "r"(h[0]), "r"(h[1]),
+                         "r"(h[2]), "r"(h[3])
+                         : "memory");
+        }
+    }
+}
+
+template <int CW>
+__device__ __forceinline__ void tmem_load_box(uint32_t taddr, uint32_t (&v)[CW]) {
+    if constexpr (CW == 16) {
+        ptx::tmem_ld_32x32b_x16(taddr, v);
+    } else if constexpr (CW == 8) {
+        ptx::tmem_ld_32x32b_x8(taddr, v);
+    } else {
+        ptx::tmem_ld_32x32b_x4(taddr, v);
+    }
+    ptx::tmem_wait_ld();
+}
+
+// Stage one output box (32 x 8*TYB cells, values v of this thread) and TMA-store it.
+// TMA clips the innermost dimension at 16-byte granularity, so the store map ends at
+// ox4 = ox & ~3 and the <= 3 interior columns [ox4, ox) are written with plain stores.
+// Called by all 128 epilogue threads; `nbox` alternates the two staging buffers.
+template <int DIMS, int TYB>
+__device__ __forceinline__ void store_box(const StepParams& p, const CUtensorMap* tmap_out,
+                                          const uint32_t (&v)[2 * TYB], uint8_t* sS,
+                                          uint32_t s_stride, int nbox, int X0, int Y0, int Z0,
+                                          int c, uint32_t q, uint32_t lane, int etid) {
+    using namespace ptx;
+    constexpr int CW = 2 * TYB;
+    const uint32_t dy = lane % 8, w4 = (lane / 8) * 4;
+    const int ox = p.gx - 2 * p.r, ox4 = ox & ~3;
+    const int bx0 = X0 + c * kBoxW;  // interior x of the box
+    if (bx0 + kBoxW > ox4 && bx0 < ox) {
+        const int dxl = static_cast<int>(q) * 4 + static_cast<int>(lane / 8);
+        const int y_lim = DIMS == 2 ? p.slow_hi : p.y_end;
+#pragma unroll
+        for (int i = 0; i < CW; ++i) {
+            const int xr = bx0 + (i & 1) * kTileW + dxl;
+            const int yr = Y0 + (i / 2) * kTileH + static_cast<int>(dy);
+            if (xr >= ox4 && xr < ox && yr < y_lim)
+                p.dst[(DIMS == 3 ? static_cast<int64_t>(Z0 + p.r) * p.plane_pitch : 0) +
+                      static_cast<int64_t>(yr + p.r) * p.row_pitch + p.left_pad + p.r + xr] =
+                    __uint_as_float(v[i]);
+        }
+    }
+    if (bx0 >= ox4) return;  // nothing for the TMA store in this box (uniform across threads)
+    const uint32_t stage = smem_u32(sS) + static_cast<uint32_t>(nbox & 1) * s_stride;
+    if (etid == 0) bulk_wait_read<1>();  // the box staged here two boxes ago has been read
+    named_bar_sync(kEpiBarrier, kEpiWarps * 32);
+#pragma unroll
+    for (int i = 0; i < CW; ++i) {
+        // local output (x, y) of D row m = 32q + lane in tile (2c + (i&1), i/2); the
+        // 16-byte chunk index is XOR-swizzled with (row % 8) as TMA SWIZZLE_128B expects
+        const uint32_t y = static_cast<uint32_t>(i / 2) * kTileH + dy;
+        const uint32_t chunk = (static_cast<uint32_t>(i & 1) * 4u + q) ^ dy;
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(stage + y * 128u + chunk * 16u + w4), "r"(v[i])
+                     : "memory");
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(kEpiBarrier, kEpiWarps * 32);
+    if (etid == 0) {
+        if (DIMS == 2)
+            tma_store_2d(tmap_out, sS + (nbox & 1) * s_stride, bx0, Y0 - p.slow_lo);  // map starts at the window
+        else
+            tma_store_3d(tmap_out, sS + (nbox & 1) * s_stride, bx0, Y0, Z0);
+        bulk_commit();
+    }
+}
+
+}  // namespace sst

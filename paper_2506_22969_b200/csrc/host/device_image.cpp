@@ -12,6 +12,7 @@
 //   col_origin (layout.cpp:162-188 restated for a shared-memory patch).
 #include <algorithm>
 #include <array>
+#include <cstdint>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -87,43 +88,67 @@ DeviceImage build_device_image(const BatchGeometry& geo_in, std::size_t rows, st
     DeviceImage img;
     img.geo = geo_in;
     BatchGeometry& g = img.geo;
-    g.k_pad = static_cast<int>((cols + 31) / 32 * 32);
+    // z_slices > 1 (3D z-streaming): A'' is cut into kz z-slices of C columns
+    // each (expand_units orders the PIT'd columns z-major, convert.cpp:376-396),
+    // every slice padded to its own K; B'' is gathered per input plane.
+    const std::size_t nsl = static_cast<std::size_t>(std::max(1, g.z_slices));
+    if (cols % nsl != 0) throw std::invalid_argument("A'' columns do not split into z slices");
+    const std::size_t C = cols / nsl;
+    if (nsl > 1 && C % 4 != 0) throw std::invalid_argument("z slice is not 4-group aligned");
+    g.k_pad = static_cast<int>((C + 31) / 32 * 32);
     const std::size_t k_pad = static_cast<std::size_t>(g.k_pad), ksteps = k_pad / 32;
     const std::size_t half_cols = cols / 2, quarter_cols = cols / 4;
 
-    // ---- A image
-    img.a_smem.assign(128 * k_pad / 2, 0);
-    for (std::size_t m = 0; m < 128; ++m)
-        for (std::size_t j = 0; j < half_cols; ++j) {
-            const std::size_t s = j / 16, jj = j % 16;
-            const std::size_t at = s * 2048 + (m / 8) * 128 + (jj / 8) * 64 + (m % 8) * 8 + jj % 8;
-            img.a_smem[at] = f32_to_f16_bits(static_cast<float>(values[m * half_cols + j]));
-        }
-
-    // ---- E words
-    img.e_words.assign(ksteps * 128, 0);
-    for (std::size_t s = 0; s < ksteps; ++s)
+    // ---- A image: slice dz occupies K steps [dz*ksteps, (dz+1)*ksteps)
+    img.a_smem.assign(nsl * 128 * k_pad / 2, 0);
+    for (std::size_t dz = 0; dz < nsl; ++dz)
         for (std::size_t m = 0; m < 128; ++m)
-            for (std::size_t gl = 0; gl < 8; ++gl) {
-                const std::size_t grp = s * 8 + gl;
-                const std::uint32_t nib = grp < quarter_cols ? (meta[m * quarter_cols + grp] & 0xfu)
-                                                            : 0x4u;  // padding: canonical {0,1}
-                const std::size_t m0 = m % 8, m1 = (m / 8) % 2, m2 = m / 16;
-                const std::size_t lane = m0 + 8 * (gl / 4) + 16 * m2;
-                img.e_words[s * 128 + lane] |= nib << (4 * ((gl % 4) + 4 * m1));
+            for (std::size_t jl = 0; jl < C / 2; ++jl) {
+                const std::size_t j = dz * (C / 2) + jl;  // stored index in the reference order
+                const std::size_t s = dz * ksteps + jl / 16, jj = jl % 16;
+                const std::size_t at = s * 2048 + (m / 8) * 128 + (jj / 8) * 64 + (m % 8) * 8 + jj % 8;
+                img.a_smem[at] = f32_to_f16_bits(static_cast<float>(values[m * half_cols + j]));
             }
 
-    // ---- K-row offsets into the shared-memory patch
+    // ---- E words
+    img.e_words.assign(nsl * ksteps * 128, 0);
+    for (std::size_t dz = 0; dz < nsl; ++dz)
+        for (std::size_t s = 0; s < ksteps; ++s)
+            for (std::size_t m = 0; m < 128; ++m)
+                for (std::size_t gl = 0; gl < 8; ++gl) {
+                    const std::size_t grp = s * 8 + gl;  // group inside the slice
+                    const std::uint32_t nib =
+                        grp < C / 4 ? (meta[m * quarter_cols + dz * (C / 4) + grp] & 0xfu)
+                                    : 0x4u;  // padding: canonical {0,1}
+                    const std::size_t m0 = m % 8, m1 = (m / 8) % 2, m2 = m / 16;
+                    const std::size_t lane = m0 + 8 * (gl / 4) + 16 * m2;
+                    img.e_words[(dz * ksteps + s) * 128 + lane] |= nib << (4 * ((gl % 4) + 4 * m1));
+                }
+
+    // ---- K-row offsets into the shared-memory patch (one slice: positions [0, C))
     const std::int32_t plane = g.patch_w * g.patch_h;
     img.koff.assign(k_pad, 0);  // zero columns read a real (finite) patch cell; A'' is 0 there
-    for (std::size_t q = 0; q < cols; ++q) {
-        const std::size_t j = col_origin[q];
-        if (j == npos) continue;
-        const std::size_t z = j / (wu * wv), u = (j % (wu * wv)) / wv, v = j % wv;
-        img.koff[q] = static_cast<std::int32_t>(z) * plane +
-                      static_cast<std::int32_t>(u) * g.patch_w + static_cast<std::int32_t>(v) +
-                      g.x_shift;
-    }
+    std::vector<std::int64_t> uv(C, -1);
+    for (std::size_t dz = 0; dz < nsl; ++dz)
+        for (std::size_t ql = 0; ql < C; ++ql) {
+            const std::size_t j = col_origin[dz * C + ql];
+            std::int64_t here = -1;
+            std::size_t z = 0;
+            if (j != npos) {
+                z = j / (wu * wv);
+                here = static_cast<std::int64_t>(j % (wu * wv));
+            }
+            if (nsl > 1) {
+                if (j != npos && z != dz) throw std::invalid_argument("z slice holds a foreign plane");
+                if (dz == 0) uv[ql] = here;
+                else if (uv[ql] != here) throw std::invalid_argument("z slices differ in (u, v) order");
+            }
+            if (dz > 0 || j == npos) continue;
+            const std::size_t u = static_cast<std::size_t>(here) / wv, v = static_cast<std::size_t>(here) % wv;
+            img.koff[ql] = static_cast<std::int32_t>(nsl > 1 ? 0 : z) * plane +
+                           static_cast<std::int32_t>(u) * g.patch_w + static_cast<std::int32_t>(v) +
+                           g.x_shift;
+        }
 
     // ---- gather schedule: partition 8-row groups into 32-row sweeps with few
     // shared-memory bank conflicts (deterministic local search)

@@ -21,6 +21,7 @@ struct BatchGeometry {
     int patch_h = 0;           // rows per plane
     int patch_planes = 1;      // kz (3D) or 1
     int k_pad = 0;             // logical K rounded to the MMA K step (32)
+    int z_slices = 1;          // 1: whole A'' per MMA pass; kz: 3D z-streaming slices
     int x_shift = 0;           // patch column of the window origin (TMA boxes start
                                // 16-byte aligned, so the patch begins lp cells early)
     int n_tiles() const { return tiles_x * tiles_y; }
