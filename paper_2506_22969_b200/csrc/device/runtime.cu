@@ -143,6 +143,7 @@ struct sst_plan {
     uint64_t launches = 0;
     int debug_mode = 0;  // SST_DEBUG_MODE (ablation experiments only)
     uint64_t fuse = 1;   // original time steps per launch
+    int load_x0 = 0;     // storage column of a batch's patch start, relative to X0
 
     ~sst_plan() {
         cudaSetDevice(device);
@@ -156,12 +157,24 @@ struct sst_plan {
         }
     }
 
+    // L2 sector promotion of TMA traffic (SST_L2_PROMO=0/64/128/256 overrides;
+    // experiments only): 128 B keeps a patch row's tail sector from dragging a
+    // neighbour's 256 B into L2 when that neighbour is not running concurrently
+    static CUtensorMapL2promotion l2_promotion() {
+        const char* e = std::getenv("SST_L2_PROMO");
+        const int v = e ? std::atoi(e) : 128;
+        return v == 0     ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+               : v == 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+               : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                          : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    }
+
     static void encode(CUtensorMap* m, int rank, void* base, const cuuint64_t* dim,
                        const cuuint64_t* stride, const cuuint32_t* box, CUtensorMapSwizzle swz) {
         cuuint32_t estride[3] = {1, 1, 1};
         const CUresult rc = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, static_cast<cuuint32_t>(rank),
                                         base, dim, stride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                        swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                        swz, l2_promotion(),
                                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (rc != CUDA_SUCCESS)
             throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(rc) + ")", false);
@@ -219,6 +232,7 @@ struct sst_plan {
         p.row_pitch = static_cast<int64_t>(storage.row_pitch);
         p.plane_pitch = static_cast<int64_t>(storage.plane_pitch);
         p.left_pad = static_cast<int32_t>(storage.left_pad);
+        p.load_x0 = load_x0;
         p.gx = gx;
         p.gy = gy;
         p.gz = gz;
@@ -291,8 +305,14 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
         if (P->gx < d->k || P->gy < d->k || P->gz < (d->dims == 3 ? d->k : 1))
             throw std::invalid_argument("grid smaller than kernel");
 
-        // storage: interior column r lands on a 16-byte boundary
-        const uint64_t lp = (4 - static_cast<uint64_t>(P->r) % 4) % 4;
+        // storage: the first interior column (r) of every row lands on a 16-byte
+        // boundary (TMA store requirement). SST_ALIGN=128 aligns it to whole L2 lines
+        // instead (measured slower on 8192^2 Box-2D9P: the patch loads then start
+        // mid-line; kept as an experiment switch)
+        const char* al = std::getenv("SST_ALIGN");
+        const uint64_t aln = (al && std::atoi(al) == 128) ? 32 : 4;  // elements
+        const uint64_t lp = (aln - static_cast<uint64_t>(P->r) % aln) % aln;
+        P->load_x0 = static_cast<int>(lp & ~uint64_t{3});  // 16-byte aligned patch start
         int max_smem = 0;
         ck(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device),
            "cudaDeviceGetAttribute");
@@ -304,11 +324,11 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
         geo.k = d->k;
         geo.tiles_x = 8;
         geo.patch_planes = d->dims == 3 ? d->k : 1;
-        // the patch is loaded from the 16-byte aligned storage column X0, i.e.
-        // lp cells left of the window origin (TMA box starts must be aligned)
-        geo.x_shift = static_cast<int>(lp);
+        // the patch is loaded from the 16-byte aligned storage column X0 + load_x0,
+        // lp & 3 cells left of the window origin (TMA box starts must be aligned)
+        geo.x_shift = static_cast<int>(lp & 3);
         geo.patch_w = static_cast<int>(sst::align_up(
-            static_cast<uint32_t>(lp + d->window_w + sst::kTileW * (geo.tiles_x - 1)), 4));
+            static_cast<uint32_t>((lp & 3) + d->window_w + sst::kTileW * (geo.tiles_x - 1)), 4));
         std::vector<std::size_t> origin(d->cols);
         for (std::size_t i = 0; i < d->cols; ++i)
             origin[i] = d->col_origin[i] == UINT64_MAX ? stensor::npos
@@ -366,7 +386,7 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
         if (const char* dm = std::getenv("SST_DEBUG_MODE")) P->debug_mode = std::atoi(dm);
 
         P->storage.left_pad = lp;
-        P->storage.row_pitch = (lp + static_cast<uint64_t>(P->gx) + 3) / 4 * 4;
+        P->storage.row_pitch = (lp + static_cast<uint64_t>(P->gx) + aln - 1) / aln * aln;
         P->storage.plane_pitch = P->storage.row_pitch * static_cast<uint64_t>(P->gy);
         P->storage.bytes = P->storage.plane_pitch * static_cast<uint64_t>(P->gz) * 4;
 

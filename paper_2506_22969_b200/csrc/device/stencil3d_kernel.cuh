@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int s = it % NP;
                     mbar_wait(&patch_empty[s], ((it / NP) & 1) ^ 1);
                     mbar_arrive_expect_tx(&patch_full[s], pbytes);
-                    tma_load_3d(sP + s * L.p_stride, &tmap_in, &patch_full[s], X0, Y0, z);
+                    tma_load_3d(sP + s * L.p_stride, &tmap_in, &patch_full[s], X0 + p.load_x0, Y0, z);
                 }
             });
         }
@@ -157,7 +157,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int zo = zi - dz;
                         if (zo < zo_a || zo > zo_b) continue;
                         const int slot = (obase + (zo - zo_a)) % NACC;
-                        for (int ks = 0; ks < ksz; ++ks) {
+                        const int nk = (p.debug_mode & 4) ? 1 : ksz;
+                        for (int ks = 0; ks < nk; ++ks) {
                             const int kk = dz * ksz + ks;  // A'' / metadata K step
                             const uint64_t ad = make_smem_desc(a0 + kk * 4096u, 128, 256);
                             const uint64_t bd = make_smem_desc(b0 + ks * 512u, 128, b_sbo);
@@ -181,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int32_t toff[GPW][8];
         tile_offsets<TYB, GPW>(gw, p.patch_w, toff);
         const uint32_t gstride = static_cast<uint32_t>(p.k_pad) * 16u;
-        const int nsweeps = active ? ksz : 0;
+        const int nsweeps = (active && !(p.debug_mode & 2)) ? ksz : 0;
         int it = 0;
         for_each_run(u0, u1, ozw, [&](int col, int zo_a, int zo_b) {
             (void)col;
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---------------------------------------------------------- epilogue
         const uint32_t q = static_cast<uint32_t>(warp % 4);
         const int etid = threadIdx.x - kEpiWarp0 * 32;
-        int o = 0, nbox = 0;
+        int o = 0;
         for_each_run(u0, u1, ozw, [&](int col, int zo_a, int zo_b) {
             int X0, Y0;
             col_xy(col, X0, Y0);
@@ -211,18 +212,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int slot = o % NACC;
                 mbar_wait(&d_full[slot], (o / NACC) & 1);
                 tc_fence_after();
-#pragma unroll 1
-                for (int c = 0; c < NBOX; ++c, ++nbox) {
-                    uint32_t v[CW];
-                    tmem_load_box<CW>(tmem + ((q * 32u) << 16) + static_cast<uint32_t>(slot * N + c * CW), v);
-                    if (c == NBOX - 1) {
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&d_empty[slot]);
-                    }
-                    store_box<3, TYB>(p, &tmap_out, v, sS, L.s_stride, nbox, X0, Y0, p.slow_lo + zo, c,
-                                      q, lane, etid);
-                }
+                uint32_t v[NBOX][CW];
+                tmem_load_batch<TYB>(tmem + ((q * 32u) << 16) + static_cast<uint32_t>(slot * N), v);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&d_empty[slot]);
+                if (!(p.debug_mode & 1))
+                    store_batch<3, TYB>(p, &tmap_out, v, sS, L.s_stride, o, X0, Y0, p.slow_lo + zo, q,
+                                        lane, etid);
             }
         });
         if (etid == 0) bulk_wait<0>();

@@ -18,6 +18,7 @@ constexpr int kTileW = 16, kTileH = 8;  // r1, r2
 constexpr int kTXB = 8;                 // tiles per batch along x (128 outputs)
 constexpr int kBoxW = 32;               // output box width (128 B, SWIZZLE_128B)
 constexpr uint32_t kEpiBarrier = 1;     // named barrier of the 4 epilogue warps
+constexpr int kStageBufs = 1;           // batch staging buffers (TMA stores in flight)
 
 struct StepParams {
     const uint4* a_img;        // A'' smem image (fp16), nks * 4096 bytes
@@ -27,6 +28,7 @@ struct StepParams {
     float* dst;                // output storage buffer (right-edge columns, see epilogue)
     int64_t row_pitch, plane_pitch;  // storage pitches (elements)
     int32_t left_pad;
+    int32_t load_x0;           // storage column of the patch start relative to X0 (16B aligned)
     int32_t gx, gy, gz;        // logical extents
     int32_t r;                 // radius
     int32_t slow_lo, slow_hi;  // window over the slowest axis (y in 2D, z in 3D), interior coords
@@ -124,53 +126,80 @@ __device__ __forceinline__ void tmem_load_box(uint32_t taddr, uint32_t (&v)[CW])
     ptx::tmem_wait_ld();
 }
 
-// Stage one output box (32 x 8*TYB cells, values v of this thread) and TMA-store it.
+// The whole accumulator of a batch (all NBOX output boxes) -> registers, then the
+// TMEM slot is handed back before any store work starts.
+template <int TYB>
+__device__ __forceinline__ void tmem_load_batch(uint32_t taddr, uint32_t (&v)[kTXB / 2][2 * TYB]) {
+#pragma unroll
+    for (int c = 0; c < kTXB / 2; ++c) {
+        if constexpr (TYB == 8) {
+            ptx::tmem_ld_32x32b_x16(taddr + c * 16, v[c]);
+        } else if constexpr (TYB == 4) {
+            ptx::tmem_ld_32x32b_x8(taddr + c * 8, v[c]);
+        } else {
+            ptx::tmem_ld_32x32b_x4(taddr + c * 4, v[c]);
+        }
+    }
+    ptx::tmem_wait_ld();
+}
+
+// Stage one batch of outputs (NBOX boxes of 32 x 8*TYB cells; this thread's values
+// v) into a 128B-swizzled smem buffer and TMA-store it: one barrier pair per batch.
 // TMA clips the innermost dimension at 16-byte granularity, so the store map ends at
 // ox4 = ox & ~3 and the <= 3 interior columns [ox4, ox) are written with plain stores.
-// Called by all 128 epilogue threads; `nbox` alternates the two staging buffers.
+// Called by all 128 epilogue threads; `nb` (batch count) cycles kStageBufs buffers.
 template <int DIMS, int TYB>
-__device__ __forceinline__ void store_box(const StepParams& p, const CUtensorMap* tmap_out,
-                                          const uint32_t (&v)[2 * TYB], uint8_t* sS,
-                                          uint32_t s_stride, int nbox, int X0, int Y0, int Z0,
-                                          int c, uint32_t q, uint32_t lane, int etid) {
+__device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorMap* tmap_out,
+                                            const uint32_t (&v)[kTXB / 2][2 * TYB], uint8_t* sS,
+                                            uint32_t s_stride, int nb, int X0, int Y0, int Z0,
+                                            uint32_t q, uint32_t lane, int etid) {
     using namespace ptx;
-    constexpr int CW = 2 * TYB;
+    constexpr int CW = 2 * TYB, NBOX = kTXB / 2;
     const uint32_t dy = lane % 8, w4 = (lane / 8) * 4;
     const int ox = p.gx - 2 * p.r, ox4 = ox & ~3;
-    const int bx0 = X0 + c * kBoxW;  // interior x of the box
-    if (bx0 + kBoxW > ox4 && bx0 < ox) {
+    if (X0 + kTXB * kTileW > ox4) {  // right-edge batch: plain stores for [ox4, ox)
         const int dxl = static_cast<int>(q) * 4 + static_cast<int>(lane / 8);
         const int y_lim = DIMS == 2 ? p.slow_hi : p.y_end;
 #pragma unroll
-        for (int i = 0; i < CW; ++i) {
-            const int xr = bx0 + (i & 1) * kTileW + dxl;
-            const int yr = Y0 + (i / 2) * kTileH + static_cast<int>(dy);
-            if (xr >= ox4 && xr < ox && yr < y_lim)
-                p.dst[(DIMS == 3 ? static_cast<int64_t>(Z0 + p.r) * p.plane_pitch : 0) +
-                      static_cast<int64_t>(yr + p.r) * p.row_pitch + p.left_pad + p.r + xr] =
-                    __uint_as_float(v[i]);
-        }
+        for (int c = 0; c < NBOX; ++c)
+#pragma unroll
+            for (int i = 0; i < CW; ++i) {
+                const int xr = X0 + c * kBoxW + (i & 1) * kTileW + dxl;
+                const int yr = Y0 + (i / 2) * kTileH + static_cast<int>(dy);
+                if (xr >= ox4 && xr < ox && yr < y_lim)
+                    p.dst[(DIMS == 3 ? static_cast<int64_t>(Z0 + p.r) * p.plane_pitch : 0) +
+                          static_cast<int64_t>(yr + p.r) * p.row_pitch + p.left_pad + p.r + xr] =
+                        __uint_as_float(v[c][i]);
+            }
     }
-    if (bx0 >= ox4) return;  // nothing for the TMA store in this box (uniform across threads)
-    const uint32_t stage = smem_u32(sS) + static_cast<uint32_t>(nbox & 1) * s_stride;
-    if (etid == 0) bulk_wait_read<1>();  // the box staged here two boxes ago has been read
+    const uint32_t buf = static_cast<uint32_t>(nb % kStageBufs) * NBOX * s_stride;
+    const uint32_t stage = smem_u32(sS) + buf;
+    if (etid == 0) bulk_wait_read<kStageBufs - 1>();  // this buffer's previous stores have read it
     named_bar_sync(kEpiBarrier, kEpiWarps * 32);
 #pragma unroll
-    for (int i = 0; i < CW; ++i) {
-        // local output (x, y) of D row m = 32q + lane in tile (2c + (i&1), i/2); the
-        // 16-byte chunk index is XOR-swizzled with (row % 8) as TMA SWIZZLE_128B expects
-        const uint32_t y = static_cast<uint32_t>(i / 2) * kTileH + dy;
-        const uint32_t chunk = (static_cast<uint32_t>(i & 1) * 4u + q) ^ dy;
-        asm volatile("st.shared.b32 [%0], %1;" ::"r"(stage + y * 128u + chunk * 16u + w4), "r"(v[i])
-                     : "memory");
-    }
+    for (int c = 0; c < NBOX; ++c)
+#pragma unroll
+        for (int i = 0; i < CW; ++i) {
+            // local output (x, y) of D row m = 32q + lane in tile (2c + (i&1), i/2); the
+            // 16-byte chunk index is XOR-swizzled with (row % 8) as TMA SWIZZLE_128B expects
+            const uint32_t y = static_cast<uint32_t>(i / 2) * kTileH + dy;
+            const uint32_t chunk = (static_cast<uint32_t>(i & 1) * 4u + q) ^ dy;
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(stage + c * s_stride + y * 128u + chunk * 16u + w4),
+                         "r"(v[c][i])
+                         : "memory");
+        }
     fence_proxy_async_smem();
     named_bar_sync(kEpiBarrier, kEpiWarps * 32);
     if (etid == 0) {
-        if (DIMS == 2)
-            tma_store_2d(tmap_out, sS + (nbox & 1) * s_stride, bx0, Y0 - p.slow_lo);  // map starts at the window
-        else
-            tma_store_3d(tmap_out, sS + (nbox & 1) * s_stride, bx0, Y0, Z0);
+#pragma unroll
+        for (int c = 0; c < NBOX; ++c) {
+            const int bx0 = X0 + c * kBoxW;
+            if (bx0 >= ox4) break;  // fully clipped
+            if (DIMS == 2)
+                tma_store_2d(tmap_out, sS + buf + c * s_stride, bx0, Y0 - p.slow_lo);  // map starts at the window
+            else
+                tma_store_3d(tmap_out, sS + buf + c * s_stride, bx0, Y0, Z0);
+        }
         bulk_commit();
     }
 }

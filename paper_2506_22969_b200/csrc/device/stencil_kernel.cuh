@@ -44,7 +44,7 @@ __host__ __device__ inline SmemLayout smem_layout_generic(int nks, int k_pad, in
     o += nbb * L.b_stride;
     L.s_stride = align_up(static_cast<uint32_t>(kBoxW * kTileH * TYB) * 4u, 1024);
     L.s = o = align_up(o, 1024);
-    o += 2 * L.s_stride;
+    o += kStageBufs * (kTXB / 2) * L.s_stride;
     L.p_stride = align_up(static_cast<uint32_t>(patch_w * patch_h * planes) * 4u, 128);
     L.p = o = align_up(o, 128);
     o += np * L.p_stride;
@@ -150,9 +150,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // window origin sits left_pad cells into the patch (gsrc has it)
                 void* dst = sP + s * L.p_stride;
                 if (DIMS == 2)
-                    tma_load_2d(dst, &tmap_in, &patch_full[s], X0, Y0);
+                    tma_load_2d(dst, &tmap_in, &patch_full[s], X0 + p.load_x0, Y0);
                 else
-                    tma_load_3d(dst, &tmap_in, &patch_full[s], X0, Y0, Z0);
+                    tma_load_3d(dst, &tmap_in, &patch_full[s], X0 + p.load_x0, Y0, Z0);
             }
         }
     } else if (warp == 1) {
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---------------------------------------------------------- epilogue
         const uint32_t q = static_cast<uint32_t>(warp % 4);
         const int etid = threadIdx.x - kEpiWarp0 * 32;  // 0..127
-        int it = 0, nbox = 0;
+        int it = 0;
         for (int b = blockIdx.x; b < p.nbatch; b += gridDim.x, ++it) {
             const int s = it & 1;
             const uint32_t ph = (it >> 1) & 1;
@@ -219,18 +219,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             batch_coords(b, X0, Y0, Z0);
             mbar_wait(&d_full[s], ph);
             tc_fence_after();
-#pragma unroll 1
-            for (int c = 0; c < NBOX; ++c, ++nbox) {
-                uint32_t v[CW];
-                tmem_load_box<CW>(tmem + ((q * 32u) << 16) + static_cast<uint32_t>(s * N + c * CW), v);
-                if (c == NBOX - 1) {  // accumulator fully read: hand it back to the MMA warp
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&d_empty[s]);
-                }
-                if (p.debug_mode & 1) continue;
-                store_box<DIMS, TYB>(p, &tmap_out, v, sS, L.s_stride, nbox, X0, Y0, Z0, c, q, lane, etid);
-            }
+            uint32_t v[NBOX][CW];
+            tmem_load_batch<TYB>(tmem + ((q * 32u) << 16) + static_cast<uint32_t>(s * N), v);
+            tc_fence_before();  // accumulator read: hand it back to the MMA warp
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&d_empty[s]);
+            if (p.debug_mode & 1) continue;
+            store_batch<DIMS, TYB>(p, &tmap_out, v, sS, L.s_stride, it, X0, Y0, Z0, q, lane, etid);
         }
         if (etid == 0) bulk_wait<0>();  // stores globally complete before the CTA retires
     }
