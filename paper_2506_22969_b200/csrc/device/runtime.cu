@@ -109,7 +109,7 @@ const Variant* variants(int& n) {
     static const Variant v[] = {
         make_variant<2, 8, 4>(), make_variant<2, 8, 3>(), make_variant<2, 4, 4>(),
         make_variant<2, 8, 2>(), make_variant<2, 4, 2>(),
-        make_stream_variant<8, 2, 3>(), make_stream_variant<4, 6, 3>(), make_stream_variant<4, 4, 3>(),
+        make_stream_variant<4, 6, 3>(), make_stream_variant<4, 4, 3>(), make_stream_variant<8, 2, 3>(),
         make_variant<3, 2, 4>(), make_variant<3, 2, 3>(), make_variant<3, 2, 2>(),
     };
     n = static_cast<int>(sizeof(v) / sizeof(v[0]));
@@ -258,12 +258,21 @@ struct sst_plan {
         return p;
     }
 
+    // streaming kernels: (row-band groups) x nbx CTAs, see stencil3d_kernel.cuh;
+    // the others: persistent CTAs striding over batches
+    int grid_size(const sst::StepParams& p) const {
+        if (variant->kz > 0) {
+            const int64_t bands = static_cast<int64_t>(p.nby) * p.nbz;
+            const int64_t groups = std::max<int64_t>(1, std::min<int64_t>(num_sms / p.nbx, bands));
+            return static_cast<int>(groups * p.nbx);
+        }
+        return std::min(p.nbatch, num_sms);
+    }
+
     void launch(int src, cudaStream_t st) {
         const sst::StepParams p = step_params(src);
         if (p.nbatch <= 0) return;
-        // streaming kernels split (column, output plane) units; others stride batches
-        const int64_t work = variant->kz > 0 ? static_cast<int64_t>(p.nbx) * p.nby * p.nbz : p.nbatch;
-        const int grid = static_cast<int>(std::min<int64_t>(work, num_sms));
+        const int grid = grid_size(p);
         if (p.slow_lo != map_lo || p.slow_hi != map_hi) make_tmaps();  // window changed
         variant->launch(grid, smem, st, tmap[src], tmap_out[src ^ 1], p);
         ck(cudaGetLastError(), "kernel launch");
@@ -440,7 +449,7 @@ sst_status sst_plan_stats_get(const sst_plan* plan, sst_plan_stats* s) {
         s->smem_bytes = plan->smem;
         const sst::StepParams p = plan->step_params(0);
         s->batches = p.nbatch;
-        s->ctas = std::min(p.nbatch, plan->num_sms);
+        s->ctas = plan->grid_size(p);
         s->launches = plan->launches;
         return SST_OK;
     } catch (...) {

@@ -106,14 +106,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
 
-    // this CTA's contiguous range of (column, output plane) units
+    // Work split. The grid is (groups x nbx) CTAs: CTA = (group, bx). All CTAs of a
+    // group walk the same contiguous range of (by, output plane) units, one per x
+    // column bx, so at any time the x-adjacent columns of a row band are in flight
+    // together: their patch rows are contiguous in HBM (DRAM page locality) and the
+    // x halos they share hit in L2.
     const int ozw = p.slow_hi - p.slow_lo;
-    const int64_t units = static_cast<int64_t>(p.nbx) * p.nby * ozw;
-    const int u0 = static_cast<int>(units * blockIdx.x / gridDim.x);
-    const int u1 = static_cast<int>(units * (blockIdx.x + 1) / gridDim.x);
-    auto col_xy = [&](int col, int& X0, int& Y0) {
-        X0 = (col % p.nbx) * (kTXB * kTileW);
-        Y0 = (col / p.nbx) * (TYB * kTileH);
+    const int bx = blockIdx.x % p.nbx, grp = blockIdx.x / p.nbx, ngrp = gridDim.x / p.nbx;
+    const int64_t units = static_cast<int64_t>(p.nby) * ozw;
+    const int u0 = static_cast<int>(units * grp / ngrp);
+    const int u1 = static_cast<int>(units * (grp + 1) / ngrp);
+    auto col_xy = [&](int by, int& X0, int& Y0) {
+        X0 = bx * (kTXB * kTileW);
+        Y0 = by * (TYB * kTileH);
     };
 
     if (warp == 0) {
