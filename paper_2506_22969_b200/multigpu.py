@@ -117,7 +117,32 @@ def exchange_halos(layout: SlabLayout, slab, pitch: int, group=None):
         ops.append(dist.P2POp(dist.irecv, view(layout.recv_down()), layout.rank + 1, group))
     if not ops:
         return []
+    if slab.is_cuda and dist.get_backend(group) != "nccl":
+        return _staged_exchange(ops, group)
     return dist.batch_isend_irecv(ops)
+
+
+class _Done:
+    def wait(self):
+        return True
+
+
+def _staged_exchange(ops, group):
+    """Host-staged exchange for CPU-side backends (gloo) with device buffers:
+    used to run the multi-rank schedule with several ranks sharing one GPU
+    (NCCL refuses two ranks per device). Synchronous: no overlap."""
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.current_stream().synchronize()
+    host = [(op, op.tensor.cpu()) for op in ops]
+    works = dist.batch_isend_irecv([dist.P2POp(op.op, h, op.peer, group) for op, h in host])
+    for w in works:
+        w.wait()
+    for op, h in host:
+        if op.op is dist.irecv:
+            op.tensor.copy_(h)
+    return [_Done()]
 
 
 class SlabStencil:
