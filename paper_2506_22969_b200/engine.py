@@ -144,12 +144,16 @@ class SparseStencil:
     def set_row_window(self, y0: int, y1: int):
         check(lib().sst_set_row_window(self._h, int(y0), int(y1)))
 
-    def apply_host(self, grid: np.ndarray, steps: int) -> np.ndarray:
-        """Host buffers in, full-size host buffer out (H2D + steps + D2H)."""
+    def apply_host(self, grid: np.ndarray, steps: int, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """Host buffers in, full-size host buffer out (H2D + steps + D2H). Pass
+        page-locked arrays (e.g. views of pinned torch tensors) for full PCIe speed."""
         g = np.ascontiguousarray(grid, dtype=np.float32)
         if list(g.shape) != list(self.grid_dims):
             raise _capi.InvalidArgument("grid shape does not match the compiled grid")
-        out = np.empty_like(g)
+        if out is None:
+            out = np.empty_like(g)
+        elif out.shape != g.shape or out.dtype != np.float32 or not out.flags["C_CONTIGUOUS"]:
+            raise _capi.InvalidArgument("out must be a C-contiguous float32 array of the grid shape")
         check(lib().sst_apply_host(self._h, g.ctypes.data_as(C.c_void_p),
                                    out.ctypes.data_as(C.c_void_p), int(steps)))
         return out

@@ -239,16 +239,17 @@ class SlabStencil:
             self.cur ^= 1
         self.eng.set_row_window(0, 0)
 
-    def apply_host(self, host: np.ndarray, steps: int) -> np.ndarray:
+    def apply_host(self, host: np.ndarray, steps: int, out: Optional[np.ndarray] = None) -> np.ndarray:
         """End to end from host memory through the public API."""
         if self.layout.world == 1:
-            return self.eng.apply_host(host, steps)
+            return self.eng.apply_host(host, steps, out=out)
         import torch
 
         self.eng.upload(np.ascontiguousarray(host, dtype=np.float32), which=0)
         self.cur = 0
         self.step(steps)
-        out = np.empty(self.local_dims, dtype=np.float32)
+        if out is None:
+            out = np.empty(self.local_dims, dtype=np.float32)
         self.eng.download(self.cur, out)
         torch.cuda.synchronize(torch.device("cuda", self.device))
         return out
