@@ -1,0 +1,48 @@
+"""Kernel ablation timing (profiling aid, not a bench): for each config, variant and
+debug mode (1 no stores, 2 no gather, 4 no MMA), time `steps` launches with CUDA
+events and print microseconds per launch. Usage:
+    python tools/ablate.py Box-3D27P 512x512x512 [variants=-1,5,6] [modes=0,1,2,4,7] [steps=50]
+"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2506_22969_b200 import SparseStencil  # noqa: E402
+from paper_2506_22969_b200.multigpu import SlabStencil  # noqa: E402
+
+name = sys.argv[1]
+dims = [int(x) for x in sys.argv[2].split("x")]
+variants = [int(v) for v in (sys.argv[3] if len(sys.argv) > 3 else "-1").split(",")]
+modes = [int(m) for m in (sys.argv[4] if len(sys.argv) > 4 else "0,1,2,4").split(",")]
+steps = int(sys.argv[5]) if len(sys.argv) > 5 else 50
+fuse = int(os.environ.get("FUSE", "1"))
+
+src = SlabStencil(name, dims, fuse=fuse).make_local_input(seed=1)
+for v in variants:
+    for m in modes:
+        if v >= 0:
+            os.environ["SST_VARIANT"] = str(v)
+        else:
+            os.environ.pop("SST_VARIANT", None)
+        os.environ["SST_DEBUG_MODE"] = str(m)
+        eng = SparseStencil(name, dims, fuse=fuse)
+        eng.bind_torch()
+        eng.upload(src, 0)
+        eng.run(3 * fuse)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        eng.run(steps * fuse)
+        b.record()
+        torch.cuda.synchronize()
+        us = a.elapsed_time(b) * 1e3 / steps
+        st = eng.stats()
+        cells = 1
+        for d in dims:
+            cells *= d
+        print(f"variant {v:2d} mode {m} : {us:8.2f} us/launch  {cells * fuse / us / 1e3:7.1f} GSt/s  "
+              f"patch {st['patch_w']}x{st['patch_h']}x{st['patch_planes']} stages {st['patch_stages']} "
+              f"ctas {st['ctas']} smem {st['smem_bytes']}", flush=True)
+        eng.close()
