@@ -49,6 +49,35 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
+// Every step kernel is launched with programmatic stream serialization: its
+// prologue (barrier init, TMEM alloc, constant staging) runs while the previous
+// step drains, and griddepcontrol.wait in the kernel orders all grid-buffer
+// accesses after that step completes. SST_PDL=0 disables it (A/B experiments).
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SST_PDL");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
+
+using KernelFn = void (*)(CUtensorMap, CUtensorMap, sst::StepParams);
+
+void launch_pdl(KernelFn fn, int grid, int smem, cudaStream_t st, const CUtensorMap& tin,
+                const CUtensorMap& tout, const sst::StepParams& p) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(sst::kThreads);
+    cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    ck(cudaLaunchKernelEx(&cfg, fn, tin, tout, p), "cudaLaunchKernelEx");
+}
+
 // One compiled instantiation of the step kernel: (dims, tile rows per batch,
 // patch pipeline depth). Plans pick the deepest variant that fits in smem.
 struct Variant {
@@ -76,7 +105,7 @@ Variant make_variant() {
     };
     v.launch = [](int grid, int smem, cudaStream_t st, const CUtensorMap& tin,
                   const CUtensorMap& tout, const sst::StepParams& p) {
-        sst::stencil_step_kernel<D, TYB, NP><<<grid, sst::kThreads, smem, st>>>(tin, tout, p);
+        launch_pdl(sst::stencil_step_kernel<D, TYB, NP>, grid, smem, st, tin, tout, p);
     };
     return v;
 }
@@ -98,7 +127,7 @@ Variant make_stream_variant() {
     };
     v.launch = [](int grid, int smem, cudaStream_t st, const CUtensorMap& tin,
                   const CUtensorMap& tout, const sst::StepParams& p) {
-        sst::stencil3d_stream_kernel<TYB, NP, KZ><<<grid, sst::kThreads, smem, st>>>(tin, tout, p);
+        launch_pdl(sst::stencil3d_stream_kernel<TYB, NP, KZ>, grid, smem, st, tin, tout, p);
     };
     return v;
 }

@@ -105,6 +105,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    grid_dep_wait();  // grid buffers only below (PDL: the prologue overlaps the previous step)
+    grid_dep_launch();
 
     // Work split. The grid is (groups x nbx) CTAs: CTA = (group, bx). All CTAs of a
     // group walk the same contiguous range of (by, output plane) units, one per x

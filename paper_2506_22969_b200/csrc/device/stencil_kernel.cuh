@@ -126,6 +126,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    // everything above touches only the plan's constants: it overlaps the previous
+    // time step's tail under PDL. The grid buffers are read / written only below.
+    grid_dep_wait();
+    grid_dep_launch();
 
     const int nbx = p.nbx, nby = p.nby;
     auto batch_coords = [&](int b, int& X0, int& Y0, int& Z0) {
