@@ -156,6 +156,10 @@ SST_API sst_status sst_run_steps(sst_plan* plan, int src, uint64_t steps, void* 
  * blocked axis (used by the multi-GPU driver to split interior / boundary
  * work); y1 <= y0 resets to the full interior. */
 SST_API sst_status sst_set_row_window(sst_plan* plan, uint64_t y0, uint64_t y1);
+/* Profiling aid: when dev_buf (device memory, 4 x u64 per CTA) is non-NULL,
+ * every following launch writes per CTA {smid, start ns, main-loop start ns,
+ * end ns} (globaltimer) at dev_buf[4 * cta]. NULL turns it off. */
+SST_API sst_status sst_plan_set_trace(sst_plan* plan, void* dev_buf);
 /* End to end from host memory: upload, run, download (full-size grid). */
 SST_API sst_status sst_apply_host(sst_plan* plan, const float* h_in, float* h_out, uint64_t steps);
 

@@ -21,7 +21,7 @@ EXPORTED = [
     "sst_compiled_perm", "sst_compiled_col_origin", "sst_compiled_matrix",
     "sst_compiled_plan_desc", "sst_plan_create", "sst_plan_destroy", "sst_plan_storage",
     "sst_plan_stats_get", "sst_plan_bind", "sst_upload", "sst_download", "sst_run_steps",
-    "sst_set_row_window", "sst_apply_host", "sst_random_grid", "sst_last_error",
+    "sst_set_row_window", "sst_plan_set_trace", "sst_apply_host", "sst_random_grid", "sst_last_error",
     "sst_device_count", "sst_version",
 ]
 
@@ -117,6 +117,7 @@ def lib() -> C.CDLL:
         "sst_download": (i32, [P, i32, P, i32, P]),
         "sst_run_steps": (i32, [P, i32, u64, P, C.POINTER(i32)]),
         "sst_set_row_window": (i32, [P, u64, u64]),
+        "sst_plan_set_trace": (i32, [P, P]),
         "sst_apply_host": (i32, [P, P, P, u64]),
         "sst_random_grid": (i32, [i32, C.POINTER(u64), u64, P]),
         "sst_last_error": (C.c_char_p, []),

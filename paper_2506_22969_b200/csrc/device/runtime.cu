@@ -79,67 +79,83 @@ void launch_pdl(KernelFn fn, int grid, int smem, cudaStream_t st, const CUtensor
 }
 
 // One compiled instantiation of the step kernel: (dims, tile rows per batch,
-// patch pipeline depth). Plans pick the deepest variant that fits in smem.
+// patch pipeline depth, A'' in TMEM or smem). Plans pick the first variant in
+// preference order whose smem and TMEM budgets fit.
 struct Variant {
     int dims, tyb, np;
-    int kz;  // 0: whole-window kernel; > 0: 3D z-streaming kernel with kz z slices
+    int kz;         // 0: whole-window kernel; > 0: 3D z-streaming kernel with kz z slices
+    bool a_tmem;    // compressed A'' in TMEM
+    int acc_cols;   // TMEM columns of the accumulator ring
     sst::SmemLayout (*layout)(int nks, int k_pad, int pw, int ph, int planes);
     void (*configure)(int smem);
     void (*launch)(int grid, int smem, cudaStream_t st, const CUtensorMap& tin,
                    const CUtensorMap& tout, const sst::StepParams& p);
 };
 
-template <int D, int TYB, int NP>
+template <int D, int TYB, int NP, bool AT>
 Variant make_variant() {
     Variant v{};
     v.dims = D;
     v.tyb = TYB;
     v.np = NP;
+    v.a_tmem = AT;
+    v.acc_cols = 2 * sst::kTXB * TYB;
     v.layout = [](int nks, int k_pad, int pw, int ph, int planes) {
-        return sst::smem_layout<TYB, NP>(nks, k_pad, pw, ph, planes);
+        return sst::smem_layout<TYB, NP, AT>(nks, k_pad, pw, ph, planes);
     };
     v.configure = [](int smem) {
-        ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP>,
+        ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
            "cudaFuncSetAttribute");
     };
     v.launch = [](int grid, int smem, cudaStream_t st, const CUtensorMap& tin,
                   const CUtensorMap& tout, const sst::StepParams& p) {
-        launch_pdl(sst::stencil_step_kernel<D, TYB, NP>, grid, smem, st, tin, tout, p);
+        launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT>, grid, smem, st, tin, tout, p);
     };
     return v;
 }
 
-template <int TYB, int NP, int KZ>
+template <int TYB, int NP, int KZ, bool AT, int NB = 2, int NACC = KZ + 1, int NS = 1>
 Variant make_stream_variant() {
     Variant v{};
     v.dims = 3;
     v.tyb = TYB;
     v.np = NP;
     v.kz = KZ;
+    v.a_tmem = AT;
+    v.acc_cols = NACC * sst::kTXB * TYB;
     v.layout = [](int nks, int k_pad, int pw, int ph, int) {
-        return sst::smem_layout_stream<TYB, NP, KZ>(nks, k_pad, pw, ph);
+        return sst::smem_layout_stream<TYB, NP, KZ, NB, NACC, NS, AT>(nks, k_pad, pw, ph);
     };
     v.configure = [](int smem) {
-        ck(cudaFuncSetAttribute(sst::stencil3d_stream_kernel<TYB, NP, KZ>,
+        ck(cudaFuncSetAttribute(sst::stencil3d_stream_kernel<TYB, NP, KZ, NB, NACC, NS, AT>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
            "cudaFuncSetAttribute");
     };
     v.launch = [](int grid, int smem, cudaStream_t st, const CUtensorMap& tin,
                   const CUtensorMap& tout, const sst::StepParams& p) {
-        launch_pdl(sst::stencil3d_stream_kernel<TYB, NP, KZ>, grid, smem, st, tin, tout, p);
+        launch_pdl(sst::stencil3d_stream_kernel<TYB, NP, KZ, NB, NACC, NS, AT>, grid, smem, st, tin, tout, p);
     };
     return v;
 }
 
-// preference order per dimensionality: 3D z-streaming first, then the deepest
-// TMA pipeline that fits (SST_VARIANT=<index> forces one, for experiments)
+// preference order per dimensionality: 3D z-streaming first, A'' in TMEM first,
+// then the deepest TMA pipeline that fits (SST_VARIANT=<index> forces one, for
+// experiments; SST_A_SMEM=1 skips the A''-in-TMEM variants)
 const Variant* variants(int& n) {
     static const Variant v[] = {
-        make_variant<2, 8, 4>(), make_variant<2, 8, 3>(), make_variant<2, 4, 4>(),
-        make_variant<2, 8, 2>(), make_variant<2, 4, 2>(),
-        make_stream_variant<4, 6, 3>(), make_stream_variant<4, 4, 3>(), make_stream_variant<8, 2, 3>(),
-        make_variant<3, 2, 4>(), make_variant<3, 2, 3>(), make_variant<3, 2, 2>(),
+        // 2D (measured order, tools/ablate.py): 0 smem-A 8x3 (Box-2D9P 8192^2: 89.6 us),
+        // 1 TMEM-A 4x4 (Star-2D13P 16384^2: 435 us vs 462 for smem-A 4x4), then the rest
+        make_variant<2, 8, 3, false>(), make_variant<2, 4, 4, true>(), make_variant<2, 8, 3, true>(),
+        make_variant<2, 4, 4, false>(), make_variant<2, 4, 2, true>(), make_variant<2, 8, 2, false>(),
+        make_variant<2, 4, 2, false>(), make_variant<2, 8, 4, false>(), make_variant<2, 8, 4, true>(),
+        // 3D z-streaming (9-15): TMEM-A TYB 4 NP 4 (Box-3D27P 512^3: 206 us vs 222 smem-A), ...
+        make_stream_variant<4, 4, 3, true>(), make_stream_variant<4, 3, 3, true>(),
+        make_stream_variant<8, 3, 3, true>(), make_stream_variant<4, 2, 3, true>(),
+        make_stream_variant<4, 6, 3, true>(), make_stream_variant<4, 4, 3, false>(),
+        make_stream_variant<8, 2, 3, false>(),
+        // 3D whole-window kernel (kz != 3 or non-streamable layouts): 16-18
+        make_variant<3, 2, 4, false>(), make_variant<3, 2, 3, false>(), make_variant<3, 2, 2, false>(),
     };
     n = static_cast<int>(sizeof(v) / sizeof(v[0]));
     return v;
@@ -156,6 +172,8 @@ struct sst_plan {
     const Variant* variant = nullptr;
     sst_storage storage{};
     int smem = 0, num_sms = 0;
+    int tmem_cols = 256;  // TMEM allocation of the chosen variant
+    unsigned long long* trace = nullptr;  // profiling: per-CTA timestamps (sst_plan_set_trace)
     // device constants
     void* d_a = nullptr;
     uint32_t* d_e = nullptr;
@@ -284,6 +302,8 @@ struct sst_plan {
         p.patch_h = img.geo.patch_h;
         p.patch_planes = img.geo.patch_planes;
         p.debug_mode = debug_mode;
+        p.tmem_cols = tmem_cols;
+        p.trace = trace;
         return p;
     }
 
@@ -395,10 +415,13 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
         const Variant* vars = variants(nvar);
         const char* force = std::getenv("SST_VARIANT");
         const int forced = force ? std::atoi(force) : -1;
+        const char* asm_env = std::getenv("SST_A_SMEM");
+        const bool no_a_tmem = asm_env && std::atoi(asm_env) != 0;
         for (int i = 0; i < nvar && !P->variant; ++i) {
             const Variant& v = vars[i];
             if (v.dims != d->dims || (forced >= 0 && i != forced)) continue;
             if (v.kz > 0 && (!can_stream || v.kz != kz)) continue;
+            if (v.a_tmem && no_a_tmem && forced < 0) continue;
             const int ph = static_cast<int>(d->window_h) + sst::kTileH * (v.tyb - 1);
             const int kp = v.kz > 0 ? k_pad_z : k_pad;
             const int nks = v.kz > 0 ? kz * k_pad_z / 32 : k_pad / 32;
@@ -406,8 +429,13 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
             const sst::SmemLayout L = v.layout(nks, kp, geo.patch_w, ph, planes);
             const int need = static_cast<int>(L.total) + 1024;  // slack for the 1 KiB base alignment
             if (need > max_smem || ph > 256) continue;
+            const uint32_t tneed =
+                sst::tmem_budget(static_cast<uint32_t>(v.acc_cols), static_cast<uint32_t>(nks), v.a_tmem).need;
+            if (tneed > 512) continue;
+            if (sst::prologue_scratch_bytes(nks, v.a_tmem) > L.gsrc - L.b) continue;
             P->variant = &v;
             P->smem = need;
+            P->tmem_cols = tneed <= 32 ? 32 : tneed <= 64 ? 64 : tneed <= 128 ? 128 : tneed <= 256 ? 256 : 512;
             geo.tiles_y = v.tyb;
             geo.patch_h = ph;
             if (v.kz > 0) {
@@ -557,6 +585,16 @@ sst_status sst_download(sst_plan* plan, int which, float* dst, int dst_on_device
         const auto st = static_cast<cudaStream_t>(stream);
         copy_dense(plan, which, nullptr, dst, false, dst_on_device != 0, st);
         if (!dst_on_device) ck(cudaStreamSynchronize(st), "cudaStreamSynchronize(download)");
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_plan_set_trace(sst_plan* plan, void* dev_buf) {
+    try {
+        if (!plan) throw std::invalid_argument("null plan");
+        plan->trace = static_cast<unsigned long long*>(dev_buf);
         return SST_OK;
     } catch (...) {
         return sstc::from_current_exception();

@@ -22,10 +22,10 @@
 
 namespace sst {
 
-template <int TYB, int NP, int KZ>
+template <int TYB, int NP, int KZ, int NB, int NACC, int NS, bool AT>
 __host__ __device__ inline SmemLayout smem_layout_stream(int nks, int k_pad, int patch_w, int patch_h) {
-    constexpr int NACC = KZ + 1;
-    return smem_layout_generic<TYB>(nks, k_pad, patch_w, patch_h, 1, NP, 2, 2 * NP + 4 + 2 * NACC);
+    return smem_layout_generic<TYB>(nks, k_pad, patch_w, patch_h, 1, NP, NB, 2 * NP + 2 * NB + 2 * NACC,
+                                    NS, AT);
 }
 
 // Iterates the runs of a CTA's unit range: calls fn(col, zo_a, zo_b) for each run
@@ -40,7 +40,10 @@ __device__ __forceinline__ void for_each_run(int u0, int u1, int ozw, Fn&& fn) {
     }
 }
 
-template <int TYB, int NP, int KZ>
+// NB: B'' ring depth, NACC (> KZ): accumulator ring, NS: output staging buffers,
+// AT: compressed A'' in TMEM instead of smem (frees smem and its bandwidth: with
+// N = 32 the per-MMA A reads were the largest smem stream of the 3D kernel).
+template <int TYB, int NP, int KZ, int NB, int NACC, int NS, bool AT>
 __global__ void __launch_bounds__(kThreads, 1)
     stencil3d_stream_kernel(const __grid_constant__ CUtensorMap tmap_in,
                             const __grid_constant__ CUtensorMap tmap_out, const StepParams p) {
@@ -49,14 +52,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int NBOX = kTXB / 2;
     constexpr int NGROUP = N / 8;
     constexpr int GPW = NGROUP >= kGatherWarps ? NGROUP / kGatherWarps : 1;
-    constexpr int NACC = KZ + 1;
     constexpr int R = (KZ - 1) / 2;
+    static_assert(NACC > KZ, "one accumulator beyond the KZ open ones");
     static_assert(N % 16 == 0 && N <= 128, "UMMA N for M=128");
-    static_assert(NACC * N <= 256, "accumulator ring must leave TMEM room for metadata");
+    static_assert(NACC * N <= 320, "accumulator ring must leave TMEM room for metadata / A''");
     using namespace ptx;
 
     extern __shared__ __align__(1024) uint8_t smem[];
-    const SmemLayout L = smem_layout_stream<TYB, NP, KZ>(p.nks, p.k_pad, p.patch_w, p.patch_h);
+    const SmemLayout L = smem_layout_stream<TYB, NP, KZ, NB, NACC, NS, AT>(p.nks, p.k_pad, p.patch_w, p.patch_h);
     uint8_t* sA = smem + L.a;
     uint8_t* sB = smem + L.b;
     uint8_t* sS = smem + L.s;
@@ -67,13 +70,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* patch_full = bars;
     uint64_t* patch_empty = bars + NP;
     uint64_t* b_full = bars + 2 * NP;
-    uint64_t* b_empty = b_full + 2;
-    uint64_t* d_full = b_full + 4;
+    uint64_t* b_empty = b_full + NB;
+    uint64_t* d_full = b_full + 2 * NB;
     uint64_t* d_empty = d_full + NACC;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem_slot);
 
     const int warp = threadIdx.x / 32;
     const uint32_t lane = lane_id();
+    const unsigned long long t_start = p.trace ? global_ns() : 0ull;
     const int ksz = p.k_pad / 32;  // K steps per z slice
 
     if (threadIdx.x == 0) {
@@ -81,7 +85,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&patch_full[s], 1);
             mbar_init(&patch_empty[s], kGatherWarps);
         }
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < NB; ++s) {
             mbar_init(&b_full[s], kGatherWarps);
             mbar_init(&b_empty[s], 1);
         }
@@ -93,20 +97,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch_desc(&tmap_in);
         tma_prefetch_desc(&tmap_out);
     }
-    if (warp == 1) tmem_alloc(tmem_slot, 512);
-    stage_constants(p, sA, sGsrc, sGdst);
+    if (warp == 1) tmem_alloc(tmem_slot, static_cast<uint32_t>(p.tmem_cols));
+    stage_constants<AT>(p, sA, sB, sGsrc, sGdst);
     fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t e_col = NACC * N;  // metadata after the accumulator ring
-    if (warp >= kEpiWarp0) store_metadata(p, tmem, e_col, static_cast<uint32_t>(warp % 4), lane);
+    const TmemCols tc = tmem_budget(NACC * N, static_cast<uint32_t>(p.nks), AT);
+    const uint32_t e_col = tc.e_col;  // metadata after the accumulator ring, then A'' (AT)
+    if (warp >= kEpiWarp0) {
+        store_metadata<AT>(p, sB, tmem, e_col, static_cast<uint32_t>(warp % 4), lane);
+        if constexpr (AT) store_a_tmem(p, sB, tmem, tc.a_col, static_cast<uint32_t>(warp % 4), lane);
+    }
+    fence_proxy_async_smem();  // scratch (generic writes / reads) is reused by TMA below
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     grid_dep_wait();  // grid buffers only below (PDL: the prologue overlaps the previous step)
     grid_dep_launch();
+    const unsigned long long t_main = p.trace ? global_ns() : 0ull;
 
     // Work split. The grid is (groups x nbx) CTAs: CTA = (group, bx). All CTAs of a
     // group walk the same contiguous range of (by, output plane) units, one per x
@@ -149,8 +159,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for_each_run(u0, u1, ozw, [&](int col, int zo_a, int zo_b) {
             (void)col;
             for (int zi = zo_a; zi <= zo_b + 2 * R; ++zi, ++it) {  // window-relative input plane
-                const int s = it & 1;
-                mbar_wait(&b_full[s], (it >> 1) & 1);
+                const int s = it % NB;
+                mbar_wait(&b_full[s], (it / NB) & 1);
                 // a new accumulator starts at dz = 0 (zo = zi): wait until it is drained
                 if (zi <= zo_b) {
                     const int o = obase + (zi - zo_a);
@@ -167,11 +177,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int nk = (p.debug_mode & 4) ? 1 : ksz;
                         for (int ks = 0; ks < nk; ++ks) {
                             const int kk = dz * ksz + ks;  // A'' / metadata K step
-                            const uint64_t ad = make_smem_desc(a0 + kk * 4096u, 128, 256);
                             const uint64_t bd = make_smem_desc(b0 + ks * 512u, 128, b_sbo);
                             const uint32_t ea = tmem + e_col + static_cast<uint32_t>(kk);
-                            mma_sp_f16(tmem + static_cast<uint32_t>(slot * N), ad, bd, ea & ~1u,
-                                       idesc | (ea & 1u), (dz > 0 || ks > 0) ? 1u : 0u);
+                            const uint32_t acc = (dz > 0 || ks > 0) ? 1u : 0u;
+                            if constexpr (AT) {
+                                mma_sp_f16_ts(tmem + static_cast<uint32_t>(slot * N),
+                                              tmem + tc.a_col + static_cast<uint32_t>(kk) * 8u, bd, ea & ~1u,
+                                              idesc | (ea & 1u), acc);
+                            } else {
+                                const uint64_t ad = make_smem_desc(a0 + kk * 4096u, 128, 256);
+                                mma_sp_f16(tmem + static_cast<uint32_t>(slot * N), ad, bd, ea & ~1u,
+                                           idesc | (ea & 1u), acc);
+                            }
                         }
                     }
                     mma_commit(&b_empty[s]);
@@ -194,9 +211,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for_each_run(u0, u1, ozw, [&](int col, int zo_a, int zo_b) {
             (void)col;
             for (int zi = zo_a; zi <= zo_b + 2 * R; ++zi, ++it) {
-                const int ps = it % NP, s = it & 1;
+                const int ps = it % NP, s = it % NB;
                 mbar_wait(&patch_full[ps], (it / NP) & 1);
-                mbar_wait(&b_empty[s], ((it >> 1) & 1) ^ 1);
+                mbar_wait(&b_empty[s], ((it / NB) & 1) ^ 1);
                 gather_batch<GPW>(smem_u32(sP + ps * L.p_stride), smem_u32(sB + s * L.b_stride),
                                   sGsrc, sGdst, nsweeps, gw, gstride, lane, toff);
                 fence_proxy_async_smem();
@@ -225,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&d_empty[slot]);
                 if (!(p.debug_mode & 1))
-                    store_batch<3, TYB>(p, &tmap_out, v, sS, L.s_stride, o, X0, Y0, p.slow_lo + zo, q,
+                    store_batch<3, TYB, NS>(p, &tmap_out, v, sS, L.s_stride, o, X0, Y0, p.slow_lo + zo, q,
                                         lane, etid);
             }
         });
@@ -234,9 +251,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     tc_fence_before();
     __syncthreads();
+    if (p.trace && threadIdx.x == 0) {
+        unsigned long long* t = p.trace + 4 * blockIdx.x;
+        t[0] = smid();
+        t[1] = t_start;
+        t[2] = t_main;
+        t[3] = global_ns();
+    }
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tmem, 512);
+        tmem_dealloc(tmem, static_cast<uint32_t>(p.tmem_cols));
     }
 }
 

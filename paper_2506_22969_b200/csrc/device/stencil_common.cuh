@@ -37,8 +37,32 @@ struct StepParams {
     int32_t k_pad;             // B'' rows per MMA pass (per z slice when streaming)
     int32_t nks;               // 32-wide K steps in the A'' image (all slices)
     int32_t patch_w, patch_h, patch_planes;
-    int32_t debug_mode;        // ablation bits (profiling only): 1 no stores, 2 no gather, 4 no MMA
+    int32_t debug_mode;        // ablation bits (profiling only): 1 no stores, 2 no gather, 4 no MMA,
+                               // 8 no right-edge plain stores
+    int32_t tmem_cols;         // TMEM allocation (power of two >= the kernel's column budget)
+    unsigned long long* trace; // profiling only (sst_plan_set_trace): per CTA {smid, t_start, t_main, t_end}
 };
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned smid() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+
+// TMEM column budget of a kernel: accumulators, then the nks metadata columns,
+// then (A in TMEM) 8 columns per K step starting on a 32-column boundary.
+struct TmemCols {
+    uint32_t e_col, a_col, need;
+};
+__host__ __device__ constexpr TmemCols tmem_budget(uint32_t acc_cols, uint32_t nks, bool a_in_tmem) {
+    const uint32_t e = acc_cols, a = (acc_cols + nks + 31u) / 32u * 32u;
+    return TmemCols{e, a, a_in_tmem ? a + nks * 8u : acc_cols + nks};
+}
 
 // tile (column n of the MMA) -> (tx, ty) of the batch: output box c (32 x-cells,
 // tiles tx = 2c, 2c+1) owns columns [c*2*TYB, (c+1)*2*TYB), n = c*2*TYB + 2*ty + (tx & 1)
@@ -49,24 +73,58 @@ __host__ __device__ inline void tile_of_column(int n, int& tx, int& ty) {
     tx = 2 * c + (m & 1);
 }
 
-// A'' image and the gather tables: global -> smem (all threads)
-__device__ __forceinline__ void stage_constants(const StepParams& p, uint8_t* sA, int32_t* sGsrc,
-                                                int32_t* sGdst) {
-    const int n16 = p.nks * 4096 / 16;
-    uint4* dstA = reinterpret_cast<uint4*>(sA);
-    for (int i = threadIdx.x; i < n16; i += kThreads) dstA[i] = p.a_img[i];
+// Prologue staging, global -> smem with all threads, coalesced 16-byte loads and
+// no intervening asm barriers (one memory round trip): the A'' image (to its smem
+// home, or to `scratch` when it goes to TMEM), the TMEM metadata words (to
+// `scratch`) and the gather tables. `scratch` is the B'' / staging / patch region,
+// idle until the main loop; the host checks it is large enough.
+template <bool AT>
+__device__ __forceinline__ void stage_constants(const StepParams& p, uint8_t* sA, uint8_t* scratch,
+                                                int32_t* sGsrc, int32_t* sGdst) {
+    const int nA = p.nks * 4096 / 16;
+    uint4* dA = reinterpret_cast<uint4*>(AT ? scratch : sA);
+    for (int i = threadIdx.x; i < nA; i += kThreads) dA[i] = p.a_img[i];
+    const int nE = p.nks * 128 / 4;
+    uint4* dE = reinterpret_cast<uint4*>(scratch + (AT ? p.nks * 4096 : 0));
+    const uint4* gE = reinterpret_cast<const uint4*>(p.e_words);
+    for (int i = threadIdx.x; i < nE; i += kThreads) dE[i] = gE[i];
     for (int i = threadIdx.x; i < p.k_pad; i += kThreads) {  // k_pad/32 sweeps x 32 lanes
         sGsrc[i] = p.gsrc[i];
         sGdst[i] = p.gdst[i];
     }
 }
+__host__ __device__ inline uint32_t prologue_scratch_bytes(int nks, bool a_in_tmem) {
+    return static_cast<uint32_t>(nks) * ((a_in_tmem ? 4096u : 0u) + 512u);
+}
 
-// 2:4 metadata -> TMEM columns [e_col, e_col + nks) (each epilogue warp its lane quarter)
-__device__ __forceinline__ void store_metadata(const StepParams& p, uint32_t tmem, uint32_t e_col,
-                                               uint32_t q, uint32_t lane) {
+// 2:4 metadata -> TMEM columns [e_col, e_col + nks) (each epilogue warp its lane
+// quarter), from the words staged in smem
+template <bool AT>
+__device__ __forceinline__ void store_metadata(const StepParams& p, const uint8_t* scratch, uint32_t tmem,
+                                               uint32_t e_col, uint32_t q, uint32_t lane) {
+    const uint32_t* sE = reinterpret_cast<const uint32_t*>(scratch + (AT ? p.nks * 4096 : 0));
     for (int ks = 0; ks < p.nks; ++ks)
-        ptx::tmem_st_32x32b_x1(tmem + ((q * 32u) << 16) + e_col + ks,
-                               p.e_words[ks * 128 + q * 32 + lane]);
+        ptx::tmem_st_32x32b_x1(tmem + ((q * 32u) << 16) + e_col + ks, sE[ks * 128 + q * 32 + lane]);
+    ptx::tmem_wait_st();
+}
+
+// Compressed A'' -> TMEM columns [a_col, a_col + 8 nks) (each epilogue warp its lane
+// quarter): lane = A row m, K step s in 8 columns, kept values (2c, 2c+1) of the
+// step packed in column c. The staged image is the UMMA K-major interleave
+// (halves: s*2048 + (m/8)*128 + (j/8)*64 + (m%8)*8 + j%8), so each TMEM word is one
+// aligned 32-bit smem load.
+__device__ __forceinline__ void store_a_tmem(const StepParams& p, const uint8_t* scratch, uint32_t tmem,
+                                             uint32_t a_col, uint32_t q, uint32_t lane) {
+    const uint32_t m = q * 32u + lane;
+    const uint32_t* a32 = reinterpret_cast<const uint32_t*>(scratch);
+    for (int s = 0; s < p.nks; ++s) {
+        uint32_t w[8];
+#pragma unroll
+        for (uint32_t c = 0; c < 8; ++c)
+            w[c] = a32[static_cast<uint32_t>(s) * 1024u + (m / 8u) * 64u + (c / 4u) * 32u + (m % 8u) * 4u +
+                       (c % 4u)];
+        ptx::tmem_st_32x32b_x8(tmem + ((q * 32u) << 16) + a_col + static_cast<uint32_t>(s) * 8u, w);
+    }
     ptx::tmem_wait_st();
 }
 
@@ -147,8 +205,8 @@ __device__ __forceinline__ void tmem_load_batch(uint32_t taddr, uint32_t (&v)[kT
 // v) into a 128B-swizzled smem buffer and TMA-store it: one barrier pair per batch.
 // TMA clips the innermost dimension at 16-byte granularity, so the store map ends at
 // ox4 = ox & ~3 and the <= 3 interior columns [ox4, ox) are written with plain stores.
-// Called by all 128 epilogue threads; `nb` (batch count) cycles kStageBufs buffers.
-template <int DIMS, int TYB>
+// Called by all 128 epilogue threads; `nb` (batch count) cycles NS buffers.
+template <int DIMS, int TYB, int NS>
 __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorMap* tmap_out,
                                             const uint32_t (&v)[kTXB / 2][2 * TYB], uint8_t* sS,
                                             uint32_t s_stride, int nb, int X0, int Y0, int Z0,
@@ -157,24 +215,9 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
     constexpr int CW = 2 * TYB, NBOX = kTXB / 2;
     const uint32_t dy = lane % 8, w4 = (lane / 8) * 4;
     const int ox = p.gx - 2 * p.r, ox4 = ox & ~3;
-    if (X0 + kTXB * kTileW > ox4) {  // right-edge batch: plain stores for [ox4, ox)
-        const int dxl = static_cast<int>(q) * 4 + static_cast<int>(lane / 8);
-        const int y_lim = DIMS == 2 ? p.slow_hi : p.y_end;
-#pragma unroll
-        for (int c = 0; c < NBOX; ++c)
-#pragma unroll
-            for (int i = 0; i < CW; ++i) {
-                const int xr = X0 + c * kBoxW + (i & 1) * kTileW + dxl;
-                const int yr = Y0 + (i / 2) * kTileH + static_cast<int>(dy);
-                if (xr >= ox4 && xr < ox && yr < y_lim)
-                    p.dst[(DIMS == 3 ? static_cast<int64_t>(Z0 + p.r) * p.plane_pitch : 0) +
-                          static_cast<int64_t>(yr + p.r) * p.row_pitch + p.left_pad + p.r + xr] =
-                        __uint_as_float(v[c][i]);
-            }
-    }
-    const uint32_t buf = static_cast<uint32_t>(nb % kStageBufs) * NBOX * s_stride;
+    const uint32_t buf = static_cast<uint32_t>(nb % NS) * NBOX * s_stride;
     const uint32_t stage = smem_u32(sS) + buf;
-    if (etid == 0) bulk_wait_read<kStageBufs - 1>();  // this buffer's previous stores have read it
+    if (etid == 0) bulk_wait_read<NS - 1>();  // this buffer's previous stores have read it
     named_bar_sync(kEpiBarrier, kEpiWarps * 32);
 #pragma unroll
     for (int c = 0; c < NBOX; ++c)
@@ -201,6 +244,29 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
                 tma_store_3d(tmap_out, sS + buf + c * s_stride, bx0, Y0, Z0);
         }
         bulk_commit();
+    }
+    // right-edge columns [ox4, ox) (<= 3): plain stores, issued after the TMA store.
+    // A thread owns x = X0 + 32c + 16 par + dxl, so at most one (c, par) of the
+    // batch falls in [ox4, ox) for it; only that branch runs (TYB stores).
+    if (X0 + kTXB * kTileW > ox4 && !(p.debug_mode & 8)) {
+        const int dxl = static_cast<int>(q) * 4 + static_cast<int>(lane / 8);
+        const int y_lim = DIMS == 2 ? p.slow_hi : p.y_end;
+        const int y0 = Y0 + static_cast<int>(dy);
+        float* rowp = p.dst + (DIMS == 3 ? static_cast<int64_t>(Z0 + p.r) * p.plane_pitch : 0) +
+                      static_cast<int64_t>(y0 + p.r) * p.row_pitch + p.left_pad + p.r + X0 + dxl;
+        const int64_t ystep = static_cast<int64_t>(kTileH) * p.row_pitch;
+#pragma unroll
+        for (int c = 0; c < NBOX; ++c)
+#pragma unroll
+            for (int par = 0; par < 2; ++par) {
+                const int xo = c * kBoxW + par * kTileW;
+                const int xr = X0 + xo + dxl;
+                if (xr >= ox4 && xr < ox) {
+#pragma unroll
+                    for (int ty = 0; ty < TYB; ++ty)
+                        if (y0 + ty * kTileH < y_lim) rowp[xo + ty * ystep] = __uint_as_float(v[c][2 * ty + par]);
+                }
+            }
     }
 }
 

@@ -22,29 +22,29 @@
 
 namespace sst {
 
-constexpr uint32_t kTmemCols = 256;
-
 struct SmemLayout {
     uint32_t a, b, b_stride, p, p_stride, s, s_stride, gsrc, gdst, bars, tmem_slot, total;
 };
 
 __host__ __device__ inline uint32_t align_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
-// Shared-memory carve-up; np / nbb = patch and B'' ring depths, nbars mbarriers.
+// Shared-memory carve-up; np / nbb / ns = patch, B'' and output-staging ring
+// depths, nbars mbarriers.
 template <int TYB>
 __host__ __device__ inline SmemLayout smem_layout_generic(int nks, int k_pad, int patch_w, int patch_h,
-                                                          int planes, int np, int nbb, int nbars) {
+                                                          int planes, int np, int nbb, int nbars,
+                                                          int ns = kStageBufs, bool a_in_tmem = false) {
     constexpr int N = kTXB * TYB;
     SmemLayout L{};
     uint32_t o = 0;
     L.a = o;
-    o += static_cast<uint32_t>(nks) * 4096u;
+    o += a_in_tmem ? 0u : static_cast<uint32_t>(nks) * 4096u;
     L.b_stride = align_up(static_cast<uint32_t>(k_pad) * N * 2u, 1024);
     L.b = o = align_up(o, 1024);
     o += nbb * L.b_stride;
     L.s_stride = align_up(static_cast<uint32_t>(kBoxW * kTileH * TYB) * 4u, 1024);
     L.s = o = align_up(o, 1024);
-    o += kStageBufs * (kTXB / 2) * L.s_stride;
+    o += ns * (kTXB / 2) * L.s_stride;
     L.p_stride = align_up(static_cast<uint32_t>(patch_w * patch_h * planes) * 4u, 128);
     L.p = o = align_up(o, 128);
     o += np * L.p_stride;
@@ -60,13 +60,14 @@ __host__ __device__ inline SmemLayout smem_layout_generic(int nks, int k_pad, in
     return L;
 }
 
-template <int TYB, int NP>
+template <int TYB, int NP, bool AT>
 __host__ __device__ inline SmemLayout smem_layout(int nks, int k_pad, int patch_w, int patch_h,
                                                   int planes) {
-    return smem_layout_generic<TYB>(nks, k_pad, patch_w, patch_h, planes, NP, 2, 2 * NP + 8);
+    return smem_layout_generic<TYB>(nks, k_pad, patch_w, patch_h, planes, NP, 2, 2 * NP + 8, kStageBufs, AT);
 }
 
-template <int DIMS, int TYB, int NP>
+// AT: compressed A'' in TMEM (tcgen05.mma.sp [a-tmem] form) instead of smem.
+template <int DIMS, int TYB, int NP, bool AT>
 __global__ void __launch_bounds__(kThreads, 1)
     stencil_step_kernel(const __grid_constant__ CUtensorMap tmap_in,
                         const __grid_constant__ CUtensorMap tmap_out, const StepParams p) {
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     using namespace ptx;
 
     extern __shared__ __align__(1024) uint8_t smem[];
-    const SmemLayout L = smem_layout<TYB, NP>(p.nks, p.k_pad, p.patch_w, p.patch_h, p.patch_planes);
+    const SmemLayout L = smem_layout<TYB, NP, AT>(p.nks, p.k_pad, p.patch_w, p.patch_h, p.patch_planes);
     uint8_t* sA = smem + L.a;
     uint8_t* sB = smem + L.b;  // 2 stages
     uint8_t* sS = smem + L.s;  // 2 output staging boxes
@@ -98,6 +99,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x / 32;
     const uint32_t lane = lane_id();
+    const unsigned long long t_start = p.trace ? global_ns() : 0ull;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NP; ++s) {
@@ -114,15 +116,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch_desc(&tmap_in);
         tma_prefetch_desc(&tmap_out);
     }
-    if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
-    stage_constants(p, sA, sGsrc, sGdst);
+    if (warp == 1) tmem_alloc(tmem_slot, static_cast<uint32_t>(p.tmem_cols));
+    stage_constants<AT>(p, sA, sB, sGsrc, sGdst);
     fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t e_col = 2 * N;  // metadata columns after the two accumulators
-    if (warp >= kEpiWarp0) store_metadata(p, tmem, e_col, static_cast<uint32_t>(warp % 4), lane);
+    // TMEM: two accumulators, the metadata columns, then (AT) the A'' operand
+    const TmemCols tc = tmem_budget(2 * N, static_cast<uint32_t>(p.nks), AT);
+    const uint32_t e_col = tc.e_col;
+    if (warp >= kEpiWarp0) {
+        store_metadata<AT>(p, sB, tmem, e_col, static_cast<uint32_t>(warp % 4), lane);
+        if constexpr (AT) store_a_tmem(p, sB, tmem, tc.a_col, static_cast<uint32_t>(warp % 4), lane);
+    }
+    fence_proxy_async_smem();  // scratch (generic writes / reads) is reused by TMA below
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -130,6 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // time step's tail under PDL. The grid buffers are read / written only below.
     grid_dep_wait();
     grid_dep_launch();
+    const unsigned long long t_main = p.trace ? global_ns() : 0ull;
 
     const int nbx = p.nbx, nby = p.nby;
     auto batch_coords = [&](int b, int& X0, int& Y0, int& Z0) {
@@ -175,11 +184,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t b0 = smem_u32(sB + s * L.b_stride);
                 const int nks = (p.debug_mode & 4) ? 1 : p.nks;
                 for (int ks = 0; ks < nks; ++ks) {
-                    const uint64_t ad = make_smem_desc(a0 + ks * 4096u, 128, 256);
                     const uint64_t bd = make_smem_desc(b0 + ks * 512u, 128, b_sbo);
                     const uint32_t ea = tmem + e_col + static_cast<uint32_t>(ks);
-                    mma_sp_f16(tmem + static_cast<uint32_t>(s * N), ad, bd, ea & ~1u,
-                               idesc | (ea & 1u), ks > 0 ? 1u : 0u);
+                    if constexpr (AT) {
+                        mma_sp_f16_ts(tmem + static_cast<uint32_t>(s * N), tmem + tc.a_col + ks * 8u, bd,
+                                      ea & ~1u, idesc | (ea & 1u), ks > 0 ? 1u : 0u);
+                    } else {
+                        const uint64_t ad = make_smem_desc(a0 + ks * 4096u, 128, 256);
+                        mma_sp_f16(tmem + static_cast<uint32_t>(s * N), ad, bd, ea & ~1u,
+                                   idesc | (ea & 1u), ks > 0 ? 1u : 0u);
+                    }
                 }
                 mma_commit(&b_empty[s]);
                 mma_commit(&d_full[s]);
@@ -229,16 +243,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&d_empty[s]);
             if (p.debug_mode & 1) continue;
-            store_batch<DIMS, TYB>(p, &tmap_out, v, sS, L.s_stride, it, X0, Y0, Z0, q, lane, etid);
+            store_batch<DIMS, TYB, kStageBufs>(p, &tmap_out, v, sS, L.s_stride, it, X0, Y0, Z0, q, lane, etid);
         }
         if (etid == 0) bulk_wait<0>();  // stores globally complete before the CTA retires
     }
 
     tc_fence_before();
     __syncthreads();
+    if (p.trace && threadIdx.x == 0) {
+        unsigned long long* t = p.trace + 4 * blockIdx.x;
+        t[0] = smid();
+        t[1] = t_start;
+        t[2] = t_main;
+        t[3] = global_ns();
+    }
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tmem, kTmemCols);
+        tmem_dealloc(tmem, static_cast<uint32_t>(p.tmem_cols));
     }
 }
 
