@@ -61,21 +61,33 @@ bool pdl_enabled() {
     return on;
 }
 
-using KernelFn = void (*)(CUtensorMap, CUtensorMap, sst::StepParams);
+using KernelFn = void (*)(sst::MapSet, sst::StepParams);
 
-void launch_pdl(KernelFn fn, int grid, int smem, cudaStream_t st, const CUtensorMap& tin,
-                const CUtensorMap& tout, const sst::StepParams& p) {
+// cooperative: a multi-step launch relies on all its CTAs being co-resident
+// (CTAs wait on each other's step flags); the attribute makes that a launch-time
+// guarantee instead of an assumption.
+void launch_pdl(KernelFn fn, int grid, int smem, cudaStream_t st, const sst::MapSet& maps,
+                const sst::StepParams& p, bool cooperative) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(grid));
     cfg.blockDim = dim3(sst::kThreads);
     cfg.dynamicSmemBytes = static_cast<size_t>(smem);
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (pdl_enabled()) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (cooperative) {
+        attr[na].id = cudaLaunchAttributeCooperative;
+        attr[na].val.cooperative = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
-    ck(cudaLaunchKernelEx(&cfg, fn, tin, tout, p), "cudaLaunchKernelEx");
+    cfg.numAttrs = static_cast<unsigned>(na);
+    ck(cudaLaunchKernelEx(&cfg, fn, maps, p), "cudaLaunchKernelEx");
 }
 
 // One compiled instantiation of the step kernel: (dims, tile rows per batch,
@@ -88,8 +100,9 @@ struct Variant {
     int acc_cols;   // TMEM columns of the accumulator ring
     sst::SmemLayout (*layout)(int nks, int k_pad, int pw, int ph, int planes);
     void (*configure)(int smem);
-    void (*launch)(int grid, int smem, cudaStream_t st, const CUtensorMap& tin,
-                   const CUtensorMap& tout, const sst::StepParams& p);
+    bool multistep;  // one launch can run many time steps (2D dataflow kernel)
+    void (*launch)(int grid, int smem, cudaStream_t st, const sst::MapSet& maps, const sst::StepParams& p,
+                   bool cooperative);
 };
 
 template <int D, int TYB, int NP, bool AT>
@@ -108,10 +121,9 @@ Variant make_variant() {
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
            "cudaFuncSetAttribute");
     };
-    v.launch = [](int grid, int smem, cudaStream_t st, const CUtensorMap& tin,
-                  const CUtensorMap& tout, const sst::StepParams& p) {
-        launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT>, grid, smem, st, tin, tout, p);
-    };
+    v.multistep = D == 2;
+    v.launch = [](int grid, int smem, cudaStream_t st, const sst::MapSet& maps, const sst::StepParams& p,
+                  bool coop) { launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT>, grid, smem, st, maps, p, coop); };
     return v;
 }
 
@@ -132,9 +144,10 @@ Variant make_stream_variant() {
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
            "cudaFuncSetAttribute");
     };
-    v.launch = [](int grid, int smem, cudaStream_t st, const CUtensorMap& tin,
-                  const CUtensorMap& tout, const sst::StepParams& p) {
-        launch_pdl(sst::stencil3d_stream_kernel<TYB, NP, KZ, NB, NACC, NS, AT>, grid, smem, st, tin, tout, p);
+    v.multistep = false;
+    v.launch = [](int grid, int smem, cudaStream_t st, const sst::MapSet& maps, const sst::StepParams& p,
+                  bool coop) {
+        launch_pdl(sst::stencil3d_stream_kernel<TYB, NP, KZ, NB, NACC, NS, AT>, grid, smem, st, maps, p, coop);
     };
     return v;
 }
@@ -182,8 +195,11 @@ struct sst_plan {
     // ping-pong storage
     float* buf[2] = {nullptr, nullptr};
     bool owns_buf = false;
-    CUtensorMap tmap[2];      // patch loads over each buffer (whole storage)
-    CUtensorMap tmap_out[2];  // output stores, clipped to the interior (and row window)
+    sst::MapSet maps{};       // in[i]: patch loads over buffer i (whole storage);
+                              // out[i]: stores into buffer i, clipped to the interior (and row window)
+    uint32_t* d_flags = nullptr;  // per-batch step counters of multi-step launches
+    int flags_n = 0;
+    uint32_t flag_base = 0;
     bool tmap_ok = false;
     int64_t map_lo = -1, map_hi = -1;  // row window the output maps were built for
     int64_t y_lo = 0, y_hi = -1;  // interior row window
@@ -198,6 +214,7 @@ struct sst_plan {
         cudaFree(d_e);
         cudaFree(d_gsrc);
         cudaFree(d_gdst);
+        cudaFree(d_flags);
         if (owns_buf) {
             cudaFree(buf[0]);
             cudaFree(buf[1]);
@@ -245,7 +262,7 @@ struct sst_plan {
             const cuuint32_t box[3] = {static_cast<cuuint32_t>(img.geo.patch_w),
                                        static_cast<cuuint32_t>(img.geo.patch_h),
                                        static_cast<cuuint32_t>(img.geo.patch_planes)};
-            encode(&tmap[i], dims, buf[i], gdim, gstride, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+            encode(&maps.in[i], dims, buf[i], gdim, gstride, box, CU_TENSOR_MAP_SWIZZLE_NONE);
             // stores: interior origin (16-byte aligned by the left pad), interior
             // extents, 2D rows restricted to the active window -> TMA clips the
             // boundary ring, ragged edges and everything outside the window
@@ -262,7 +279,7 @@ struct sst_plan {
                                         static_cast<cuuint64_t>(gz - 2 * r)};
             const cuuint32_t obox[3] = {static_cast<cuuint32_t>(sst::kBoxW),
                                         static_cast<cuuint32_t>(tiles_y * sst::kTileH), 1u};
-            encode(&tmap_out[i], dims, base, odim, gstride, obox, CU_TENSOR_MAP_SWIZZLE_128B);
+            encode(&maps.out[i], dims, base, odim, gstride, obox, CU_TENSOR_MAP_SWIZZLE_128B);
         }
         map_lo = lo;
         map_hi = hi;
@@ -275,7 +292,12 @@ struct sst_plan {
         p.e_words = d_e;
         p.gsrc = d_gsrc;
         p.gdst = d_gdst;
-        p.dst = buf[src ^ 1];
+        p.buf[0] = buf[0];
+        p.buf[1] = buf[1];
+        p.src = src;
+        p.nsteps = 1;
+        p.flags = d_flags;
+        p.flag_base = flag_base;
         p.row_pitch = static_cast<int64_t>(storage.row_pitch);
         p.plane_pitch = static_cast<int64_t>(storage.plane_pitch);
         p.left_pad = static_cast<int32_t>(storage.left_pad);
@@ -318,14 +340,46 @@ struct sst_plan {
         return std::min(p.nbatch, num_sms);
     }
 
-    void launch(int src, cudaStream_t st) {
-        const sst::StepParams p = step_params(src);
-        if (p.nbatch <= 0) return;
+    // Launch `nsteps` operator applications starting from buffer src; returns the
+    // buffer holding the result. Multi-step launches need the full window and a
+    // multi-step variant (SST_MULTISTEP=0 forces one launch per step).
+    int launch(int src, uint64_t nsteps, cudaStream_t st) {
+        sst::StepParams p = step_params(src);
+        if (p.nbatch <= 0 || nsteps == 0) return src;
         const int grid = grid_size(p);
         if (p.slow_lo != map_lo || p.slow_hi != map_hi) make_tmaps();  // window changed
-        variant->launch(grid, smem, st, tmap[src], tmap_out[src ^ 1], p);
-        ck(cudaGetLastError(), "kernel launch");
-        ++launches;
+        const char* ms_e = std::getenv("SST_MULTISTEP");  // read per call (tests toggle it)
+        const bool ms_env = !(ms_e && std::atoi(ms_e) == 0);
+        const bool full = !(y_hi > y_lo);
+        const bool multi = ms_env && variant->multistep && full && nsteps > 1;
+        if (multi && flags_n < p.nbatch) {
+            cudaFree(d_flags);
+            d_flags = nullptr;
+            ck(cudaMalloc(&d_flags, static_cast<size_t>(p.nbatch) * 4), "cudaMalloc(flags)");
+            ck(cudaMemsetAsync(d_flags, 0, static_cast<size_t>(p.nbatch) * 4, st), "cudaMemsetAsync(flags)");
+            flags_n = p.nbatch;
+            flag_base = 0;
+        }
+        int cur = src;
+        uint64_t left = nsteps;
+        while (left > 0) {
+            // chunks keep flag counters far from wrap-around between resets
+            const uint64_t chunk = multi ? std::min<uint64_t>(left, 1u << 16) : 1;
+            p = step_params(cur);
+            p.nsteps = static_cast<int32_t>(chunk);
+            p.flags = d_flags;
+            p.flag_base = flag_base;
+            variant->launch(grid, smem, st, maps, p, multi);
+            ck(cudaGetLastError(), "kernel launch");
+            ++launches;
+            if (multi) {  // per-CTA progress counters advance by nper iterations per step
+                const uint64_t nper = (static_cast<uint64_t>(p.nbatch) + grid - 1) / grid;
+                flag_base += static_cast<uint32_t>(nper * chunk);
+            }
+            cur = (cur + static_cast<int>(chunk & 1)) & 1;
+            left -= chunk;
+        }
+        return cur;
     }
 };
 
@@ -621,11 +675,7 @@ sst_status sst_run_steps(sst_plan* plan, int src, uint64_t steps, void* stream, 
         const auto st = static_cast<cudaStream_t>(stream);
         if (steps % plan->fuse != 0)
             throw std::invalid_argument("steps must be a multiple of the fusion factor");
-        int cur = src;
-        for (uint64_t t = 0; t < steps / plan->fuse; ++t) {
-            plan->launch(cur, st);
-            cur ^= 1;
-        }
+        const int cur = plan->launch(src, steps / plan->fuse, st);
         if (dst_out) *dst_out = cur;
         return SST_OK;
     } catch (...) {
@@ -648,11 +698,7 @@ sst_status sst_apply_host(sst_plan* plan, const float* h_in, float* h_out, uint6
         // identical boundary ring in both buffers (device-side copy)
         ck(cudaMemcpyAsync(plan->buf[1], plan->buf[0], plan->storage.bytes, cudaMemcpyDeviceToDevice, st),
            "cudaMemcpyAsync(ring)");
-        int cur = 0;
-        for (uint64_t t = 0; t < steps / plan->fuse; ++t) {
-            plan->launch(cur, st);
-            cur ^= 1;
-        }
+        const int cur = plan->launch(0, steps / plan->fuse, st);
         copy_dense(plan, cur, nullptr, h_out, false, false, st);
         ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
         return SST_OK;

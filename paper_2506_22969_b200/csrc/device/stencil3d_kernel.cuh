@@ -45,8 +45,7 @@ __device__ __forceinline__ void for_each_run(int u0, int u1, int ozw, Fn&& fn) {
 // N = 32 the per-MMA A reads were the largest smem stream of the 3D kernel).
 template <int TYB, int NP, int KZ, int NB, int NACC, int NS, bool AT>
 __global__ void __launch_bounds__(kThreads, 1)
-    stencil3d_stream_kernel(const __grid_constant__ CUtensorMap tmap_in,
-                            const __grid_constant__ CUtensorMap tmap_out, const StepParams p) {
+    stencil3d_stream_kernel(const __grid_constant__ MapSet maps, const StepParams p) {
     constexpr int N = kTXB * TYB;
     constexpr int CW = 2 * TYB;
     constexpr int NBOX = kTXB / 2;
@@ -94,8 +93,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&d_empty[s], kEpiWarps);
         }
         fence_mbar_init();
-        tma_prefetch_desc(&tmap_in);
-        tma_prefetch_desc(&tmap_out);
+        tma_prefetch_desc(&maps.in[p.src]);
+        tma_prefetch_desc(&maps.out[p.src ^ 1]);
     }
     if (warp == 1) tmem_alloc(tmem_slot, static_cast<uint32_t>(p.tmem_cols));
     stage_constants<AT>(p, sA, sB, sGsrc, sGdst);
@@ -123,6 +122,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // column bx, so at any time the x-adjacent columns of a row band are in flight
     // together: their patch rows are contiguous in HBM (DRAM page locality) and the
     // x halos they share hit in L2.
+    const CUtensorMap* tmap_in = &maps.in[p.src];  // one time step per launch
+    const CUtensorMap* tmap_out = &maps.out[p.src ^ 1];
     const int ozw = p.slow_hi - p.slow_lo;
     const int bx = blockIdx.x % p.nbx, grp = blockIdx.x / p.nbx, ngrp = gridDim.x / p.nbx;
     const int64_t units = static_cast<int64_t>(p.nby) * ozw;
@@ -146,7 +147,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int s = it % NP;
                     mbar_wait(&patch_empty[s], ((it / NP) & 1) ^ 1);
                     mbar_arrive_expect_tx(&patch_full[s], pbytes);
-                    tma_load_3d(sP + s * L.p_stride, &tmap_in, &patch_full[s], X0 + p.load_x0, Y0, z);
+                    tma_load_3d(sP + s * L.p_stride, tmap_in, &patch_full[s], X0 + p.load_x0, Y0, z);
                 }
             });
         }
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&d_empty[slot]);
                 if (!(p.debug_mode & 1))
-                    store_batch<3, TYB, NS>(p, &tmap_out, v, sS, L.s_stride, o, X0, Y0, p.slow_lo + zo, q,
+                    store_batch<3, TYB, NS>(p, tmap_out, buf_of(p, p.src ^ 1), v, sS, L.s_stride, o, X0, Y0, p.slow_lo + zo, q,
                                         lane, etid);
             }
         });

@@ -20,12 +20,22 @@ constexpr int kBoxW = 32;               // output box width (128 B, SWIZZLE_128B
 constexpr uint32_t kEpiBarrier = 1;     // named barrier of the 4 epilogue warps
 constexpr int kStageBufs = 1;           // batch staging buffers (TMA stores in flight)
 
+// Load (patch) and store (interior) tensor maps of both ping-pong buffers.
+struct MapSet {
+    CUtensorMap in[2];
+    CUtensorMap out[2];
+};
+
 struct StepParams {
     const uint4* a_img;        // A'' smem image (fp16), nks * 4096 bytes
     const uint32_t* e_words;   // [nks][128]
     const int32_t* gsrc;       // [k_pad/32][32] patch byte offset of the lane's B'' row
     const int32_t* gdst;       // [k_pad/32][32] byte offset of that row in an 8-tile group
-    float* dst;                // output storage buffer (right-edge columns, see epilogue)
+    float* buf[2];             // ping-pong storage buffers (right-edge columns, see epilogue)
+    int32_t src;               // buffer holding the input of the launch's first step
+    int32_t nsteps;            // time steps (operator applications) in this launch
+    uint32_t* flags;           // [nbatch] per-batch step counters (multi-step launches)
+    uint32_t flag_base;        // counter value meaning "step 0 of this launch not yet done"
     int64_t row_pitch, plane_pitch;  // storage pitches (elements)
     int32_t left_pad;
     int32_t load_x0;           // storage column of the patch start relative to X0 (16B aligned)
@@ -42,6 +52,10 @@ struct StepParams {
     int32_t tmem_cols;         // TMEM allocation (power of two >= the kernel's column budget)
     unsigned long long* trace; // profiling only (sst_plan_set_trace): per CTA {smid, t_start, t_main, t_end}
 };
+
+__device__ __forceinline__ float* buf_of(const StepParams& p, int i) {
+    return (i & 1) ? p.buf[1] : p.buf[0];  // select, not a dynamic param-space index
+}
 
 __device__ __forceinline__ unsigned long long global_ns() {
     unsigned long long t;
@@ -207,7 +221,7 @@ __device__ __forceinline__ void tmem_load_batch(uint32_t taddr, uint32_t (&v)[kT
 // ox4 = ox & ~3 and the <= 3 interior columns [ox4, ox) are written with plain stores.
 // Called by all 128 epilogue threads; `nb` (batch count) cycles NS buffers.
 template <int DIMS, int TYB, int NS>
-__device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorMap* tmap_out,
+__device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorMap* tmap_out, float* dst,
                                             const uint32_t (&v)[kTXB / 2][2 * TYB], uint8_t* sS,
                                             uint32_t s_stride, int nb, int X0, int Y0, int Z0,
                                             uint32_t q, uint32_t lane, int etid) {
@@ -215,6 +229,31 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
     constexpr int CW = 2 * TYB, NBOX = kTXB / 2;
     const uint32_t dy = lane % 8, w4 = (lane / 8) * 4;
     const int ox = p.gx - 2 * p.r, ox4 = ox & ~3;
+    // right-edge columns [ox4, ox) (<= 3): plain stores. A thread owns
+    // x = X0 + 32c + 16 par + dxl, so at most one (c, par) of the batch falls in
+    // [ox4, ox) for it; only that branch runs (TYB stores). They precede the
+    // staging barriers below, so a flag published after this batch's TMA stores
+    // complete also covers them.
+    if (X0 + kTXB * kTileW > ox4 && !(p.debug_mode & 8)) {
+        const int dxl = static_cast<int>(q) * 4 + static_cast<int>(lane / 8);
+        const int y_lim = DIMS == 2 ? p.slow_hi : p.y_end;
+        const int y0 = Y0 + static_cast<int>(dy);
+        float* rowp = dst + (DIMS == 3 ? static_cast<int64_t>(Z0 + p.r) * p.plane_pitch : 0) +
+                      static_cast<int64_t>(y0 + p.r) * p.row_pitch + p.left_pad + p.r + X0 + dxl;
+        const int64_t ystep = static_cast<int64_t>(kTileH) * p.row_pitch;
+#pragma unroll
+        for (int c = 0; c < NBOX; ++c)
+#pragma unroll
+            for (int par = 0; par < 2; ++par) {
+                const int xo = c * kBoxW + par * kTileW;
+                const int xr = X0 + xo + dxl;
+                if (xr >= ox4 && xr < ox) {
+#pragma unroll
+                    for (int ty = 0; ty < TYB; ++ty)
+                        if (y0 + ty * kTileH < y_lim) rowp[xo + ty * ystep] = __uint_as_float(v[c][2 * ty + par]);
+                }
+            }
+    }
     const uint32_t buf = static_cast<uint32_t>(nb % NS) * NBOX * s_stride;
     const uint32_t stage = smem_u32(sS) + buf;
     if (etid == 0) bulk_wait_read<NS - 1>();  // this buffer's previous stores have read it
@@ -244,29 +283,6 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
                 tma_store_3d(tmap_out, sS + buf + c * s_stride, bx0, Y0, Z0);
         }
         bulk_commit();
-    }
-    // right-edge columns [ox4, ox) (<= 3): plain stores, issued after the TMA store.
-    // A thread owns x = X0 + 32c + 16 par + dxl, so at most one (c, par) of the
-    // batch falls in [ox4, ox) for it; only that branch runs (TYB stores).
-    if (X0 + kTXB * kTileW > ox4 && !(p.debug_mode & 8)) {
-        const int dxl = static_cast<int>(q) * 4 + static_cast<int>(lane / 8);
-        const int y_lim = DIMS == 2 ? p.slow_hi : p.y_end;
-        const int y0 = Y0 + static_cast<int>(dy);
-        float* rowp = p.dst + (DIMS == 3 ? static_cast<int64_t>(Z0 + p.r) * p.plane_pitch : 0) +
-                      static_cast<int64_t>(y0 + p.r) * p.row_pitch + p.left_pad + p.r + X0 + dxl;
-        const int64_t ystep = static_cast<int64_t>(kTileH) * p.row_pitch;
-#pragma unroll
-        for (int c = 0; c < NBOX; ++c)
-#pragma unroll
-            for (int par = 0; par < 2; ++par) {
-                const int xo = c * kBoxW + par * kTileW;
-                const int xr = X0 + xo + dxl;
-                if (xr >= ox4 && xr < ox) {
-#pragma unroll
-                    for (int ty = 0; ty < TYB; ++ty)
-                        if (y0 + ty * kTileH < y_lim) rowp[xo + ty * ystep] = __uint_as_float(v[c][2 * ty + par]);
-                }
-            }
     }
 }
 

@@ -66,16 +66,52 @@ __host__ __device__ inline SmemLayout smem_layout(int nks, int k_pad, int patch_
     return smem_layout_generic<TYB>(nks, k_pad, patch_w, patch_h, planes, NP, 2, 2 * NP + 8, kStageBufs, AT);
 }
 
+// Multi-step dataflow. Every CTA walks the same number of iterations per step
+// (nper = ceil(nbatch / grid); CTAs with one batch fewer run a no-op iteration) and
+// publishes a progress counter: flags[cta] = flag_base + iterations whose stores
+// are complete. Batch b of step t >= 1 reads outputs of step t - 1 of batches up
+// to b + nbx + 1 (its 3 x 3 neighbourhood), each processed at step-(t-1) iteration
+// <= (b + nbx + 1) / grid by its owner; so it may load once EVERY counter reached
+// flag_base + (t - 1) nper + min(nper, (b + nbx + 1) / grid + 1). The producer warp
+// keeps the minimum over all counters cached and refreshes it (one warp-wide
+// sweep) only when a batch needs more: in steady state about once per step.
+__device__ __forceinline__ uint32_t refresh_min(const StepParams& p, uint32_t need, uint32_t lane,
+                                                uint32_t& polls) {
+    for (;;) {
+        int32_t worst = 0x7fffffff;
+        for (int o = static_cast<int>(lane); o < static_cast<int>(gridDim.x); o += 32)
+            worst = min(worst, static_cast<int32_t>(ptx::ld_relaxed_gpu(p.flags + o) - need));
+        for (int sh = 16; sh > 0; sh >>= 1) worst = min(worst, __shfl_xor_sync(0xffffffffu, worst, sh));
+        if (worst >= 0) {
+            if (lane == 1) ptx::fence_acq_rel_gpu();  // acquire; lane 0 (TMA issuer) never fences
+            __syncwarp();
+            return need + static_cast<uint32_t>(worst);
+        }
+        ++polls;
+        ptx::nanosleep(128);
+    }
+}
+
 // AT: compressed A'' in TMEM (tcgen05.mma.sp [a-tmem] form) instead of smem.
+//
+// One launch runs p.nsteps time steps (persistent CTAs; 2D, full window). Step t
+// reads buffer (src + t) & 1 and writes the other one. There is no grid-wide
+// barrier between steps: batch b's epilogue publishes flags[b] = flag_base + t + 1
+// once its step-t stores are complete, and the producer waits for the 3 x 3
+// neighbourhood's flags before loading b's patch for step t + 1. That ordering also
+// covers the write-after-read on the ping-pong buffer (a neighbour publishes only
+// after it loaded its step-t patch). CTAs walk batches in the same order every
+// step, so in steady state the flags are long set when checked: no per-step
+// launch, prologue or tail.
 template <int DIMS, int TYB, int NP, bool AT>
 __global__ void __launch_bounds__(kThreads, 1)
-    stencil_step_kernel(const __grid_constant__ CUtensorMap tmap_in,
-                        const __grid_constant__ CUtensorMap tmap_out, const StepParams p) {
+    stencil_step_kernel(const __grid_constant__ MapSet maps, const StepParams p) {
     constexpr int N = kTXB * TYB;
     constexpr int CW = 2 * TYB;          // MMA columns per output box
     constexpr int NBOX = kTXB / 2;       // output boxes per batch
     constexpr int NGROUP = N / 8;        // 8-tile B'' groups
     constexpr int GPW = NGROUP >= kGatherWarps ? NGROUP / kGatherWarps : 1;
+    constexpr int PUB_LAG = 2;           // newest store groups not waited for when publishing
     static_assert(N % 16 == 0 && N <= 128, "UMMA N for M=128");
     static_assert(NGROUP % kGatherWarps == 0 || NGROUP < kGatherWarps, "group split");
     using namespace ptx;
@@ -84,7 +120,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const SmemLayout L = smem_layout<TYB, NP, AT>(p.nks, p.k_pad, p.patch_w, p.patch_h, p.patch_planes);
     uint8_t* sA = smem + L.a;
     uint8_t* sB = smem + L.b;  // 2 stages
-    uint8_t* sS = smem + L.s;  // 2 output staging boxes
+    uint8_t* sS = smem + L.s;  // output staging
     uint8_t* sP = smem + L.p;  // NP stages
     int32_t* sGsrc = reinterpret_cast<int32_t*>(smem + L.gsrc);
     int32_t* sGdst = reinterpret_cast<int32_t*>(smem + L.gdst);
@@ -113,8 +149,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&d_empty[s], kEpiWarps);
         }
         fence_mbar_init();
-        tma_prefetch_desc(&tmap_in);
-        tma_prefetch_desc(&tmap_out);
+        for (int i = 0; i < 2; ++i) {
+            tma_prefetch_desc(&maps.in[i]);
+            tma_prefetch_desc(&maps.out[i]);
+        }
     }
     if (warp == 1) tmem_alloc(tmem_slot, static_cast<uint32_t>(p.tmem_cols));
     stage_constants<AT>(p, sA, sB, sGsrc, sGdst);
@@ -135,48 +173,82 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     // everything above touches only the plan's constants: it overlaps the previous
-    // time step's tail under PDL. The grid buffers are read / written only below.
+    // launch's tail under PDL. The grid buffers are read / written only below.
     grid_dep_wait();
     grid_dep_launch();
     const unsigned long long t_main = p.trace ? global_ns() : 0ull;
 
     const int nbx = p.nbx, nby = p.nby;
+    const int G = static_cast<int>(gridDim.x);
+    // iteration j = (step t, k): batch blockIdx.x + k * G, the same batches every step;
+    // k beyond this CTA's batches is a no-op iteration (uniform nper for the counters)
+    const int nper = (p.nbatch + G - 1) / G;
+    const int total = nper * p.nsteps;
+    auto batch_of = [&](int j, int& t, int& b) {
+        t = j / nper;
+        b = static_cast<int>(blockIdx.x) + (j - t * nper) * G;
+    };
     auto batch_coords = [&](int b, int& X0, int& Y0, int& Z0) {
         X0 = (b % nbx) * (kTXB * kTileW);
         Y0 = ((b / nbx) % nby) * (TYB * kTileH) + (DIMS == 2 ? p.slow_lo : 0);
         Z0 = b / (nbx * nby) + (DIMS == 3 ? p.slow_lo : 0);
     };
+    const bool multi = p.nsteps > 1;
 
     if (warp == 0) {
         // ------------------------------------------------------ TMA producer
-        if (elect_one()) {
-            const uint32_t pbytes = static_cast<uint32_t>(p.patch_w * p.patch_h * p.patch_planes) * 4u;
-            int it = 0;
-            for (int b = blockIdx.x; b < p.nbatch; b += gridDim.x, ++it) {
-                const int s = it % NP;
-                const uint32_t ph = (it / NP) & 1;
-                int X0, Y0, Z0;
-                batch_coords(b, X0, Y0, Z0);
+        // (the whole warp walks the loop: lane 0 issues, all lanes refresh counters)
+        const uint32_t pbytes = static_cast<uint32_t>(p.patch_w * p.patch_h * p.patch_planes) * 4u;
+        uint32_t polls = 0, known = p.flag_base;  // min over all progress counters seen
+        int r = 0;                                // real (non no-op) iterations
+        for (int j = 0; j < total; ++j) {
+            int t, b, X0, Y0, Z0;
+            batch_of(j, t, b);
+            if (b >= p.nbatch) continue;
+            batch_coords(b, X0, Y0, Z0);
+            bool refreshed = false;
+            if (t > 0) {
+                const int kneed = min(nper, (min(b + nbx + 1, p.nbatch - 1)) / G + 1);
+                const uint32_t need = p.flag_base + static_cast<uint32_t>((t - 1) * nper + kneed);
+                if (static_cast<int32_t>(known - need) < 0) {
+                    known = refresh_min(p, need, lane, polls);
+                    refreshed = true;
+                }
+            }
+            if (lane == 0) {
+                const int s = r % NP;
+                const uint32_t ph = (r / NP) & 1;
                 mbar_wait(&patch_empty[s], ph ^ 1);
+                if (refreshed) fence_proxy_async_global();  // acquired data -> TMA reads
                 mbar_arrive_expect_tx(&patch_full[s], pbytes);
                 // storage column X0 is 16-byte aligned (TMA requirement); the
                 // window origin sits left_pad cells into the patch (gsrc has it)
                 void* dst = sP + s * L.p_stride;
+                const CUtensorMap* tin = &maps.in[(p.src + t) & 1];
                 if (DIMS == 2)
-                    tma_load_2d(dst, &tmap_in, &patch_full[s], X0 + p.load_x0, Y0);
+                    tma_load_2d(dst, tin, &patch_full[s], X0 + p.load_x0, Y0);
                 else
-                    tma_load_3d(dst, &tmap_in, &patch_full[s], X0 + p.load_x0, Y0, Z0);
+                    tma_load_3d(dst, tin, &patch_full[s], X0 + p.load_x0, Y0, Z0);
             }
+            __syncwarp();
+            ++r;
         }
+        if (lane == 0) tmem_slot[1] = polls;  // profiling (trace): counter sweeps that found a CTA behind
     } else if (warp == 1) {
         // -------------------------------------------------------- MMA issuer
         const uint32_t idesc = make_idesc_f16(128, N, true, 0, 1);
         const uint32_t b_sbo = static_cast<uint32_t>(p.k_pad) * 16u;
         const uint32_t a0 = smem_u32(sA);
-        int it = 0;
-        for (int b = blockIdx.x; b < p.nbatch; b += gridDim.x, ++it) {
-            const int s = it & 1;
-            const uint32_t ph = (it >> 1) & 1;
+        int r = 0;
+        for (int j = 0; j < total; ++j, ++r) {
+            int t, b;
+            batch_of(j, t, b);
+            if (b >= p.nbatch) {
+                --r;
+                continue;
+            }
+            const int s = r & 1;
+            const uint32_t ph = (r >> 1) & 1;
             mbar_wait(&b_full[s], ph);
             mbar_wait(&d_empty[s], ph ^ 1);
             tc_fence_after();
@@ -207,15 +279,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         int32_t toff[GPW][8];
         tile_offsets<TYB, GPW>(gw, p.patch_w, toff);
         const uint32_t gstride = static_cast<uint32_t>(p.k_pad) * 16u;  // bytes per 8-tile group
-        int it = 0;
-        for (int b = blockIdx.x; b < p.nbatch; b += gridDim.x, ++it) {
-            const int ps = it % NP;
-            const uint32_t pph = (it / NP) & 1;
-            const int s = it & 1;
-            const uint32_t ph = (it >> 1) & 1;
+        const int nsweeps = (active && !(p.debug_mode & 2)) ? p.k_pad / 32 : 0;
+        int r = 0;
+        for (int j = 0; j < total; ++j, ++r) {
+            int t, b;
+            batch_of(j, t, b);
+            if (b >= p.nbatch) {
+                --r;
+                continue;
+            }
+            const int ps = r % NP;
+            const uint32_t pph = (r / NP) & 1;
+            const int s = r & 1;
+            const uint32_t ph = (r >> 1) & 1;
             mbar_wait(&patch_full[ps], pph);
             mbar_wait(&b_empty[s], ph ^ 1);
-            const int nsweeps = (active && !(p.debug_mode & 2)) ? p.k_pad / 32 : 0;
             gather_batch<GPW>(smem_u32(sP + ps * L.p_stride), smem_u32(sB + s * L.b_stride), sGsrc,
                               sGdst, nsweeps, gw, gstride, lane, toff);
             fence_proxy_async_smem();  // generic-proxy writes -> tensor-core reads
@@ -229,30 +307,69 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---------------------------------------------------------- epilogue
         const uint32_t q = static_cast<uint32_t>(warp % 4);
         const int etid = threadIdx.x - kEpiWarp0 * 32;  // 0..127
-        int it = 0;
-        for (int b = blockIdx.x; b < p.nbatch; b += gridDim.x, ++it) {
-            const int s = it & 1;
-            const uint32_t ph = (it >> 1) & 1;
-            int X0, Y0, Z0;
+        // progress publication (thread etid 0, which commits the TMA store groups):
+        // iterations [0, committed) have committed stores, [0, published) are
+        // published. Publishing needs the stores complete (bulk wait) and a
+        // gpu-scope release, which also waits for this thread's newer stores, so it
+        // is batched: every PUB_EVERY iterations (lagging PUB_LAG), and whenever the
+        // epilogue has waited 2 us for an accumulator (so a stalled CTA never holds
+        // back progress it has made: no circular wait between CTAs).
+        constexpr int PUB_EVERY = 32;
+        int committed = 0, published = 0, r = 0;
+        auto publish = [&](int upto) {
+            fence_proxy_async_global();
+            fence_acq_rel_gpu();
+            st_relaxed_gpu(p.flags + blockIdx.x, p.flag_base + static_cast<uint32_t>(upto));
+            published = upto;
+        };
+        for (int j = 0; j < total; ++j) {
+            int t, b, X0, Y0, Z0;
+            batch_of(j, t, b);
+            if (b >= p.nbatch) {  // no-op iteration: nothing to store
+                committed = j + 1;
+                continue;
+            }
             batch_coords(b, X0, Y0, Z0);
-            mbar_wait(&d_full[s], ph);
+            const int s = r & 1;
+            const uint32_t ph = (r >> 1) & 1;
+            ++r;
+            if (multi && etid == 0) {
+                const unsigned long long t0 = global_ns();
+                while (!mbar_try_wait(&d_full[s], ph)) {
+                    if (published < committed && global_ns() - t0 > 2000ull) {
+                        bulk_wait<0>();
+                        publish(committed);
+                    }
+                }
+            } else {
+                mbar_wait(&d_full[s], ph);
+            }
             tc_fence_after();
             uint32_t v[NBOX][CW];
             tmem_load_batch<TYB>(tmem + ((q * 32u) << 16) + static_cast<uint32_t>(s * N), v);
             tc_fence_before();  // accumulator read: hand it back to the MMA warp
             __syncwarp();
             if (lane == 0) mbar_arrive(&d_empty[s]);
-            if (p.debug_mode & 1) continue;
-            store_batch<DIMS, TYB, kStageBufs>(p, &tmap_out, v, sS, L.s_stride, it, X0, Y0, Z0, q, lane, etid);
+            if (!(p.debug_mode & 1))
+                store_batch<DIMS, TYB, kStageBufs>(p, &maps.out[(p.src + t + 1) & 1], buf_of(p, p.src + t + 1),
+                                                   v, sS, L.s_stride, r - 1, X0, Y0, Z0, q, lane, etid);
+            committed = j + 1;
+            if (multi && etid == 0 && committed - published >= PUB_EVERY + PUB_LAG) {
+                bulk_wait<PUB_LAG>();
+                publish(committed - PUB_LAG);
+            }
         }
-        if (etid == 0) bulk_wait<0>();  // stores globally complete before the CTA retires
+        if (etid == 0) {
+            bulk_wait<0>();  // stores globally complete before the CTA retires
+            if (multi) publish(committed);
+        }
     }
 
     tc_fence_before();
     __syncthreads();
     if (p.trace && threadIdx.x == 0) {
         unsigned long long* t = p.trace + 4 * blockIdx.x;
-        t[0] = smid();
+        t[0] = smid() | (static_cast<unsigned long long>(tmem_slot[1]) << 32);
         t[1] = t_start;
         t[2] = t_main;
         t[3] = global_ns();

@@ -153,7 +153,9 @@ def test_torch_device_buffers_and_launch_count(gpu):
     eng.upload(src, 0)
     before = eng.stats()["launches"]
     dst = eng.run(7, src=0)
-    assert eng.stats()["launches"] - before == 7 and dst == 1
+    # 2D: one multi-step launch runs all 7 time steps (per-batch dataflow, no
+    # grid-wide barrier); the result lands in the other buffer after an odd count
+    assert eng.stats()["launches"] - before == 1 and dst == 1
     out = torch.empty(dims, dtype=torch.float32, device="cuda")
     eng.download(dst, out)
     torch.cuda.synchronize()
@@ -237,3 +239,32 @@ def test_every_variant_bit_exact(gpu, monkeypatch, variant):
         want = want.astype(np.float32).astype(np.float64)
         ulp = np.spacing(np.abs(want).astype(np.float32)).astype(np.float64)
         assert np.all(np.abs(got - want) <= ulp), (name, variant, np.abs(got - want).max())
+
+
+# The multi-step dataflow launch (one launch, T steps, cross-CTA progress counters)
+# must equal T single-step launches bitwise: same arithmetic per step, so any
+# ordering bug (a batch loading a neighbour's halo before it was stored) shows up
+# as a mismatch. Shapes cover grids with fewer batches than SMs, a single batch
+# row or column, ragged edges, and many steps.
+@pytest.mark.parametrize("name,dims,steps", [
+    ("Box-2D9P", (1030, 2050), 40), ("Heat-2D", (64, 4000), 31), ("Star-2D13P", (700, 300), 12),
+    ("Box-2D9P", (4000, 150), 33), ("Heat-2D", (40, 40), 9), ("Box-2D49P", (517, 1031), 10),
+    ("Box-2D9P", (2048, 2048), 200),
+])
+def test_multistep_launch_equals_single_steps(gpu, monkeypatch, name, dims, steps):
+    g = oracle.random_grid(dims, seed=21).astype(np.float32)
+
+    def go(multistep):
+        monkeypatch.setenv("SST_MULTISTEP", "1" if multistep else "0")
+        eng = SparseStencil(name, list(dims))
+        try:
+            before = eng.stats()["launches"]
+            out = eng.apply_host(g, steps)
+            return out, eng.stats()["launches"] - before
+        finally:
+            eng.close()
+
+    multi, n_multi = go(True)
+    single, n_single = go(False)
+    assert n_multi == 1 and n_single == steps
+    assert np.array_equal(multi, single)

@@ -18,6 +18,7 @@ dims = [int(x) for x in sys.argv[2].split("x")]
 if len(sys.argv) > 3 and int(sys.argv[3]) >= 0:
     os.environ["SST_VARIANT"] = sys.argv[3]
 launches = int(sys.argv[4]) if len(sys.argv) > 4 else 5
+steps = int(sys.argv[5]) if len(sys.argv) > 5 else 1  # time steps per launch (multi-step kernel)
 src = SlabStencil(name, dims).make_local_input(seed=1)
 eng = SparseStencil(name, dims)
 eng.bind_torch()
@@ -28,9 +29,11 @@ eng.run(3)
 torch.cuda.synchronize()
 check(lib().sst_plan_set_trace(eng._h, C.c_void_p(buf.data_ptr())))
 for i in range(launches):
-    eng.run(1, src=i & 1)
+    eng.run(steps, src=(i * steps) & 1)
     torch.cuda.synchronize()
     t = buf.view(ctas, 4).cpu()
+    spins = (t[:, 0] >> 32)
+    t[:, 0] &= 0xffffffff
     t0 = int(t[:, 1].min())
     start = (t[:, 1] - t0).double() / 1e3
     main = (t[:, 2] - t0).double() / 1e3
@@ -38,7 +41,8 @@ for i in range(launches):
     work = end - main
     print(f"launch {i}: span {float(end.max()):.1f} us  start max {float(start.max()):.1f}  "
           f"prologue mean {float((main - start).mean()):.2f} max {float((main - start).max()):.2f}  "
-          f"work min {float(work.min()):.1f} mean {float(work.mean()):.1f} max {float(work.max()):.1f}")
+          f"work min {float(work.min()):.1f} mean {float(work.mean()):.1f} max {float(work.max()):.1f}  "
+          f"dep polls behind: total {int(spins.sum())} max {int(spins.max())}")
     if i == launches - 1:
         order = torch.argsort(work, descending=True)
         print("slowest CTAs (cta, sm, work us):",
