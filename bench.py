@@ -318,7 +318,11 @@ def run_engine(args, cfg, cfg_name):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
-                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "algorithmic_bytes_per_step": alg_bytes,
+                     "launch_steps": (operator_steps // launches) if launches else None,
+                     "per": ("operator step: one launch runs all timed steps (2D multi-step kernel); achieved = "
+                             "8 B x interior cells / (launch time / steps), traffic = ncu DRAM bytes / steps")
+                            if launches and operator_steps // launches > 1 else "launch (one operator step)",
                      "kernel": "sst::stencil3d_stream_kernel" if len(dims) == 3
                      else "sst::stencil_step_kernel"},
         "e2e": e2e,

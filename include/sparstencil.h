@@ -23,6 +23,9 @@
  *                          with ping-pong buffers; replaces the step loop of
  *                          direct_apply (stencil.hpp:72, stencil.cpp:239-268)
  *   sst_apply_host         direct_apply(spec, grid, steps) end to end from host memory
+ *   sst_run_compile        run_compile(CompileRequest) (pipeline.hpp:14-46, pipeline.cpp:52-198):
+ *                          report.json / a2.s24 / lut.bin, desk-scale verification on the GPU
+ *   sst_explore            explore_layouts (perf.hpp:45-51), the CLI's `explore` table
  */
 #ifndef SPARSTENCIL_H_
 #define SPARSTENCIL_H_
@@ -162,6 +165,49 @@ SST_API sst_status sst_set_row_window(sst_plan* plan, uint64_t y0, uint64_t y1);
 SST_API sst_status sst_plan_set_trace(sst_plan* plan, void* dev_buf);
 /* End to end from host memory: upload, run, download (full-size grid). */
 SST_API sst_status sst_apply_host(sst_plan* plan, const float* h_in, float* h_out, uint64_t steps);
+
+/* ------------------------------------------------------- run_compile */
+
+/* Mirrors stensor::CompileRequest (pipeline.hpp:16-27) plus the verification device. */
+typedef struct sst_compile_request {
+    const char* stencil;        /* preset name or spec document */
+    const uint64_t* grid_dims;  /* slowest..fastest */
+    int32_t ndims;
+    const char* hw;             /* hardware preset name or descriptor document; NULL = a100-sparse */
+    int32_t r1, r2;             /* > 0: fixed morph factors (r2 ignored in 1D); 0: explore */
+    int32_t r_max;              /* exploration bound per factor; 0 = 16 */
+    uint64_t fuse;              /* temporal fusion factor; 0 or 1 = none */
+    int32_t precision;          /* 0 = exact64, 1 = round16 */
+    uint64_t seed;              /* verification grid seed; 0 = 1 */
+    const char* out_dir;        /* artefact directory; NULL or "" = none written */
+    int32_t verify;             /* 1: desk-scale verification (<= 256 per axis) on `device` */
+    int32_t device;
+    int32_t corrupt_permutation; /* test hook of the failure path (conversion-failed report) */
+} sst_compile_request;
+
+typedef struct sst_compile_summary {
+    int32_t ok;                 /* verified / unverified-scale / unverified-skipped */
+    int32_t r1, r2, used_blossom;
+    uint64_t p, align_cols, n_mma, issued_mma, m_prime, k_prime, n_prime;
+    double t_compute, t_memory, t_total, model_gstencil;
+    double max_abs_err, max_rel_err, verify_seconds;
+    char status[32];            /* verification.status */
+} sst_compile_summary;
+
+typedef struct sst_compile_result sst_compile_result;
+SST_API sst_status sst_run_compile(const sst_compile_request* req, sst_compile_result** out);
+SST_API void sst_compile_result_destroy(sst_compile_result* r);
+SST_API sst_status sst_compile_result_summary(const sst_compile_result* r, sst_compile_summary* s);
+/* report.json text (no terminating NUL counted in *len; buf may be NULL to query) */
+SST_API sst_status sst_compile_result_report(const sst_compile_result* r, char* buf, size_t cap, size_t* len);
+/* lut.bin bytes (docs/formats.md:65-72) */
+SST_API sst_status sst_compile_result_lut(const sst_compile_result* r, uint8_t* buf, size_t cap, size_t* len);
+
+/* explore_layouts ranking (perf.cpp:93-154): rows of 9 doubles
+ * {r1, r2, t_compute, t_memory, t_total, n_mma, m', k', n'}, best first.
+ * *len receives the number of doubles. */
+SST_API sst_status sst_explore(const char* stencil, const uint64_t* grid_dims, int ndims, const char* hw,
+                               uint64_t fuse, int r_max, double* buf, size_t cap, size_t* len);
 
 /* ----------------------------------------------------------------- misc */
 /* Synthetic input: stensor::random_grid (stencil.hpp:84-85; mt19937_64(seed),

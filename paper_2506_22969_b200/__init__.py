@@ -3,8 +3,10 @@ operators executed with tcgen05.mma.sp on sm_100a, behind the C ABI in
 include/sparstencil.h. See DESIGN.md."""
 from ._capi import (CudaFailure, InvalidArgument, LogicError, NoDevice, OutOfRange,
                     SparStencilError, lib)
-from .engine import (Compiled, SparseStencil, preset_names, sparse_apply, valid_core)
+from .engine import (Compiled, SparseStencil, explore, preset_names, run_compile, sparse_apply,
+                     valid_core)
 
-__all__ = ["Compiled", "SparseStencil", "sparse_apply", "preset_names", "valid_core", "lib",
+__all__ = ["Compiled", "SparseStencil", "sparse_apply", "run_compile", "explore", "preset_names",
+           "valid_core", "lib",
            "SparStencilError", "InvalidArgument", "LogicError", "OutOfRange", "CudaFailure",
            "NoDevice"]

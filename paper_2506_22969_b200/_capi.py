@@ -22,7 +22,8 @@ EXPORTED = [
     "sst_compiled_plan_desc", "sst_plan_create", "sst_plan_destroy", "sst_plan_storage",
     "sst_plan_stats_get", "sst_plan_bind", "sst_upload", "sst_download", "sst_run_steps",
     "sst_set_row_window", "sst_plan_set_trace", "sst_apply_host", "sst_random_grid", "sst_last_error",
-    "sst_device_count", "sst_version",
+    "sst_device_count", "sst_version", "sst_run_compile", "sst_compile_result_destroy",
+    "sst_compile_result_summary", "sst_compile_result_report", "sst_compile_result_lut", "sst_explore",
 ]
 
 
@@ -86,6 +87,23 @@ class PlanStats(C.Structure):
                 ("launches", C.c_uint64)]
 
 
+class CompileRequest(C.Structure):
+    _fields_ = [("stencil", C.c_char_p), ("grid_dims", C.POINTER(C.c_uint64)), ("ndims", C.c_int32),
+                ("hw", C.c_char_p), ("r1", C.c_int32), ("r2", C.c_int32), ("r_max", C.c_int32),
+                ("fuse", C.c_uint64), ("precision", C.c_int32), ("seed", C.c_uint64),
+                ("out_dir", C.c_char_p), ("verify", C.c_int32), ("device", C.c_int32),
+                ("corrupt_permutation", C.c_int32)]
+
+
+class CompileSummary(C.Structure):
+    _fields_ = [("ok", C.c_int32), ("r1", C.c_int32), ("r2", C.c_int32), ("used_blossom", C.c_int32),
+                ("p", C.c_uint64), ("align_cols", C.c_uint64), ("n_mma", C.c_uint64),
+                ("issued_mma", C.c_uint64), ("m_prime", C.c_uint64), ("k_prime", C.c_uint64),
+                ("n_prime", C.c_uint64), ("t_compute", C.c_double), ("t_memory", C.c_double),
+                ("t_total", C.c_double), ("model_gstencil", C.c_double), ("max_abs_err", C.c_double),
+                ("max_rel_err", C.c_double), ("verify_seconds", C.c_double), ("status", C.c_char * 32)]
+
+
 _lib = None
 
 
@@ -123,6 +141,12 @@ def lib() -> C.CDLL:
         "sst_last_error": (C.c_char_p, []),
         "sst_device_count": (i32, []),
         "sst_version": (C.c_char_p, []),
+        "sst_run_compile": (i32, [C.POINTER(CompileRequest), C.POINTER(P)]),
+        "sst_compile_result_destroy": (None, [P]),
+        "sst_compile_result_summary": (i32, [P, C.POINTER(CompileSummary)]),
+        "sst_compile_result_report": (i32, [P, P, sz, C.POINTER(sz)]),
+        "sst_compile_result_lut": (i32, [P, P, sz, C.POINTER(sz)]),
+        "sst_explore": (i32, [C.c_char_p, C.POINTER(u64), i32, C.c_char_p, u64, i32, P, sz, C.POINTER(sz)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -9,10 +9,15 @@
 #include "capi_internal.hpp"
 #include "sparstencil.h"
 #include "stensor/hwmodel.hpp"
+#include "stensor/pipeline.hpp"
 #include "stensor/morph.hpp"
 #include "stensor/s24.hpp"
 #include "stensor/sparsify.hpp"
 #include "stensor/spec.hpp"
+
+struct sst_compile_result {
+    stensor::CompileResult res;
+};
 
 struct sst_compiled {
     stensor::StencilSpec spec;
@@ -63,6 +68,14 @@ stensor::StencilSpec resolve_stencil(const char* text) {
     if (stensor::is_preset(s)) return stensor::stencil_preset(s);
     if (s.find('=') != std::string::npos) return stensor::parse_stencil_spec(s);
     throw std::invalid_argument("unknown stencil preset: " + s);
+}
+
+stensor::HardwareDescriptor resolve_hw(const char* text) {
+    const std::string s = text ? text : "a100-sparse";
+    for (const auto& n : stensor::hw_preset_names())
+        if (n == s) return stensor::hw_preset(s);
+    if (s.find('=') != std::string::npos) return stensor::parse_hw_descriptor(s);
+    throw std::invalid_argument("unknown hardware preset: " + s);
 }
 
 template <class T>
@@ -216,6 +229,110 @@ sst_status sst_random_grid(int ndims, const uint64_t* dims, uint64_t seed, float
         const stensor::Grid g = stensor::random_grid(d, seed);
         for (std::size_t i = 0; i < g.values.size(); ++i) out[i] = static_cast<float>(g.values[i]);
         return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_run_compile(const sst_compile_request* q, sst_compile_result** out) {
+    try {
+        if (!q || !out) throw std::invalid_argument("null argument");
+        *out = nullptr;
+        if (!q->grid_dims || q->ndims < 1 || q->ndims > 3) throw std::invalid_argument("bad grid");
+        stensor::CompileRequest req;
+        req.spec = resolve_stencil(q->stencil);
+        req.grid_dims.assign(q->grid_dims, q->grid_dims + q->ndims);
+        req.hw = resolve_hw(q->hw);
+        if (q->r1 > 0) {
+            req.r1 = q->r1;
+            req.r2 = q->r2 > 0 ? q->r2 : 1;
+        }
+        if (q->r_max > 0) req.r_max = q->r_max;
+        req.fuse = q->fuse > 1 ? q->fuse : 1;
+        req.precision = q->precision ? stensor::Precision::round16 : stensor::Precision::exact64;
+        req.seed = q->seed ? q->seed : 1;
+        if (q->out_dir) req.out_dir = q->out_dir;
+        req.verify = q->verify != 0;
+        req.device = q->device;
+        req.corrupt_permutation = q->corrupt_permutation != 0;
+        auto r = std::make_unique<sst_compile_result>();
+        r->res = stensor::run_compile(req);
+        *out = r.release();
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+void sst_compile_result_destroy(sst_compile_result* r) { delete r; }
+
+sst_status sst_compile_result_summary(const sst_compile_result* r, sst_compile_summary* s) {
+    try {
+        if (!r || !s) throw std::invalid_argument("null argument");
+        const auto& R = r->res;
+        *s = sst_compile_summary{};
+        s->ok = R.ok ? 1 : 0;
+        s->r1 = R.plan.layout.r1;
+        s->r2 = R.plan.layout.r2;
+        s->used_blossom = R.plan.used_blossom ? 1 : 0;
+        s->p = R.plan.p;
+        s->align_cols = R.plan.align_cols;
+        s->n_mma = R.perf.n_mma;
+        s->issued_mma = R.issued_mma;
+        s->m_prime = R.plan.layout.a.rows;
+        s->k_prime = R.plan.layout.a.cols;
+        s->n_prime = R.plan.layout.n_prime;
+        s->t_compute = R.perf.t_compute;
+        s->t_memory = R.perf.t_memory;
+        s->t_total = R.perf.t_total;
+        s->model_gstencil = R.model_gstencil;
+        s->max_abs_err = R.verification.max_abs_err;
+        s->max_rel_err = R.verification.max_rel_err;
+        s->verify_seconds = R.emulation_seconds;
+        std::strncpy(s->status, R.verification.status.c_str(), sizeof(s->status) - 1);
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_compile_result_report(const sst_compile_result* r, char* buf, size_t cap, size_t* len) {
+    try {
+        if (!r) throw std::invalid_argument("null result");
+        const std::string& t = r->res.report_json;
+        std::vector<char> v(t.begin(), t.end());
+        return copy_out(v, buf, cap, len);
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_compile_result_lut(const sst_compile_result* r, uint8_t* buf, size_t cap, size_t* len) {
+    try {
+        if (!r) throw std::invalid_argument("null result");
+        const std::string t = stensor::lut_bytes(r->res.plan.lut);
+        std::vector<uint8_t> v(t.begin(), t.end());
+        return copy_out(v, buf, cap, len);
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_explore(const char* stencil, const uint64_t* grid_dims, int ndims, const char* hw, uint64_t fuse,
+                       int r_max, double* buf, size_t cap, size_t* len) {
+    try {
+        if (!grid_dims || ndims < 1 || ndims > 3) throw std::invalid_argument("bad grid");
+        stensor::StencilSpec spec = resolve_stencil(stencil);
+        if (fuse > 1) spec = stensor::fuse_time_steps(spec, fuse);
+        const std::vector<std::size_t> dims(grid_dims, grid_dims + ndims);
+        const int rm = r_max > 0 ? r_max : 16;
+        const auto ex = stensor::explore_layouts(resolve_hw(hw), spec, dims, rm, rm);
+        std::vector<double> v;
+        for (const auto& e : ex.ranked)
+            for (double x : {double(e.r1), double(e.r2), e.t_compute, e.t_memory, e.t_total, double(e.n_mma),
+                             double(e.m_prime), double(e.k_prime), double(e.n_prime)})
+                v.push_back(x);
+        return copy_out(v, buf, cap, len);
     } catch (...) {
         return sstc::from_current_exception();
     }

@@ -219,3 +219,58 @@ def sparse_apply(stencil: str, grid: np.ndarray, steps: int, device: int = 0,
         return valid_core(full, steps, eng.r).astype(np.float64)
     finally:
         eng.close()
+
+
+def run_compile(stencil: str, grid_dims: Sequence[int], hw: str = "a100-sparse", r1: int = 0, r2: int = 0,
+                r_max: int = 16, fuse: int = 1, precision: str = "exact64", seed: int = 1,
+                out_dir: Optional[str] = None, verify: bool = True, device: int = 0,
+                corrupt_permutation: bool = False) -> dict:
+    """Mirror of stensor::run_compile (pipeline.hpp:14-46). Returns the summary,
+    the report.json text and the lut.bin bytes; writes report.json / a2.s24 /
+    lut.bin to `out_dir` when given. The desk-scale verification (<= 256 per
+    axis) runs on the GPU (`verify=False` skips it: status "unverified-skipped")."""
+    if precision not in ("exact64", "round16"):
+        raise _capi.InvalidArgument("precision must be exact64 or round16")
+    L = lib()
+    dims = (C.c_uint64 * len(grid_dims))(*[int(d) for d in grid_dims])
+    q = _capi.CompileRequest(stencil.encode(), dims, len(grid_dims), hw.encode() if hw else None, int(r1),
+                             int(r2), int(r_max), int(fuse), 1 if precision == "round16" else 0, int(seed),
+                             out_dir.encode() if out_dir else None, 1 if verify else 0, int(device),
+                             1 if corrupt_permutation else 0)
+    h = C.c_void_p()
+    check(L.sst_run_compile(C.byref(q), C.byref(h)))
+    try:
+        sm = _capi.CompileSummary()
+        check(L.sst_compile_result_summary(h, C.byref(sm)))
+        out = {f: getattr(sm, f) for f, _ in _capi.CompileSummary._fields_}
+        out["status"] = sm.status.decode()
+        out["ok"] = bool(sm.ok)
+        n = C.c_size_t()
+        check(L.sst_compile_result_report(h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        check(L.sst_compile_result_report(h, buf, n.value, C.byref(n)))
+        out["report"] = buf.raw[:n.value].decode()
+        check(L.sst_compile_result_lut(h, None, 0, C.byref(n)))
+        lb = (C.c_uint8 * n.value)()
+        check(L.sst_compile_result_lut(h, lb, n.value, C.byref(n)))
+        out["lut"] = bytes(lb)
+        return out
+    finally:
+        L.sst_compile_result_destroy(h)
+
+
+def explore(stencil: str, grid_dims: Sequence[int], hw: str = "a100-sparse", fuse: int = 1,
+            r_max: int = 16) -> list[dict]:
+    """Mirror of stensor::explore_layouts (perf.hpp:45-51): ranked (r1, r2) candidates."""
+    L = lib()
+    dims = (C.c_uint64 * len(grid_dims))(*[int(d) for d in grid_dims])
+    n = C.c_size_t()
+    check(L.sst_explore(stencil.encode(), dims, len(grid_dims), hw.encode(), int(fuse), int(r_max), None, 0,
+                        C.byref(n)))
+    buf = np.empty(n.value, dtype=np.float64)
+    check(L.sst_explore(stencil.encode(), dims, len(grid_dims), hw.encode(), int(fuse), int(r_max),
+                        buf.ctypes.data_as(C.c_void_p), n.value, C.byref(n)))
+    keys = ["r1", "r2", "t_compute", "t_memory", "t_total", "n_mma", "m_prime", "k_prime", "n_prime"]
+    rows = buf.reshape(-1, 9)
+    return [{k: (int(v) if k in ("r1", "r2", "n_mma", "m_prime", "k_prime", "n_prime") else float(v))
+             for k, v in zip(keys, r)} for r in rows]

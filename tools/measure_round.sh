@@ -1,0 +1,17 @@
+#!/bin/bash
+# Round measurement: every bench config, the reference arm, the ncu launch list of
+# the default bench command and one full ncu capture of each dominant kernel.
+# Usage (under gpurun): bash tools/measure_round.sh <outdir under gpurun_out>
+out=${1:-gpurun_out/round}
+mkdir -p $out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active --format=csv > $out/gpu.csv
+for c in box2d heat2d star2d heat3d box3d box3d1024; do
+  timeout 600 python bench.py --config $c > $out/bench_$c.json 2> $out/bench_$c.err
+done
+timeout 300 python bench.py --impl reference > $out/bench_reference.json 2> $out/bench_reference.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches_box2d.csv \
+  python bench.py --steps 8 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:stencil_step -s 1 -c 1 \
+  -o $out/prof_box2d python bench.py --steps 4 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:stencil3d -s 3 -c 1 \
+  -o $out/prof_box3d python bench.py --config box3d --steps 4 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
