@@ -4,8 +4,8 @@ CUDA runtime/kernels behind the C ABI in include/sparstencil.h).
     python -m paper_2506_22969_b200.build        # or build() from __graft_entry__
 
 Incremental by mtime; objects under paper_2506_22969_b200/build/ (git-ignored),
-the shared library next to this file so it travels to the GPU box with the
-repo snapshot. cudart is linked statically and the driver API is resolved at
+the shared library next to this file (and the `sstensor` CLI under bin/) so
+they travel to the GPU box with the repo snapshot. cudart is linked statically and the driver API is resolved at
 run time (cudaGetDriverEntryPoint), so the library loads on a CPU-only host.
 """
 from __future__ import annotations
@@ -20,6 +20,7 @@ REPO = PKG.parent
 CSRC = PKG / "csrc"
 OBJ = PKG / "build"
 LIB = PKG / "libsparstencil.so"
+CLI = PKG / "bin" / "sstensor"
 
 NVCC = os.environ.get("NVCC", "nvcc")
 CXX = os.environ.get("CXX", "g++")
@@ -63,6 +64,14 @@ def build(verbose: bool = False, force: bool = False) -> Path:
             _run([NVCC, *NVFLAGS, *INCLUDES, "-c", src, "-o", o], verbose)
     if force or _stale(LIB, objs):
         _run([NVCC, "-shared", *ARCH, "-cudart", "static", "-o", LIB, *objs], verbose)
+    # the CLI (reference tools/main.cpp) links the same objects statically
+    cli_src = CSRC / "cli" / "sstensor.cpp"
+    cli_obj = OBJ / "sstensor.o"
+    if force or _stale(cli_obj, [cli_src, *HEADERS, __file__]):
+        _run([CXX, *CXXFLAGS, *INCLUDES, "-I/usr/local/cuda/include", "-c", cli_src, "-o", cli_obj], verbose)
+    CLI.parent.mkdir(exist_ok=True)
+    if force or _stale(CLI, [*objs, cli_obj]):
+        _run([NVCC, *ARCH, "-cudart", "static", "-o", CLI, cli_obj, *objs], verbose)
     return LIB
 
 
