@@ -145,12 +145,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // input (storage) planes of outputs zo_a..zo_b: zo_a .. zo_b + 2R
                 for (int z = p.slow_lo + zo_a; z <= p.slow_lo + zo_b + 2 * R; ++z, ++it) {
                     const int s = it % NP;
-                    mbar_wait(&patch_empty[s], ((it / NP) & 1) ^ 1);
+                    if (p.debug_mode & 16) {  // TMA-only: the producer recycles its own ring
+                        if (it >= NP) mbar_wait(&patch_full[s], ((it / NP) - 1) & 1);
+                    } else {
+                        mbar_wait(&patch_empty[s], ((it / NP) & 1) ^ 1);
+                    }
                     mbar_arrive_expect_tx(&patch_full[s], pbytes);
                     tma_load_3d(sP + s * L.p_stride, tmap_in, &patch_full[s], X0 + p.load_x0, Y0, z);
                 }
             });
+            if (p.debug_mode & 16)
+                for (int j = (it > NP ? it - NP : 0); j < it; ++j) mbar_wait(&patch_full[j % NP], (j / NP) & 1);
         }
+    } else if (p.debug_mode & 16) {
+        // TMA-only ablation: the other roles idle
     } else if (warp == 1) {
         // -------------------------------------------------------- MMA issuer
         const uint32_t idesc = make_idesc_f16(128, N, true, 0, 1);
@@ -171,14 +179,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (elect_one()) {
                     const uint32_t b0 = smem_u32(sB + s * L.b_stride);
 #pragma unroll
-                    for (int dz = 0; dz < KZ; ++dz) {
-                        const int zo = zi - dz;
-                        if (zo < zo_a || zo > zo_b) continue;
-                        const int slot = (obase + (zo - zo_a)) % NACC;
-                        const int nk = (p.debug_mode & 4) ? 1 : ksz;
-                        for (int ks = 0; ks < nk; ++ks) {
+                    // K step outer, z slice inner: consecutive MMAs go to the KZ different
+                    // accumulators (independent), not KZ chains of dependent ones
+                    const int nk = (p.debug_mode & 4) ? 1 : ksz;
+                    for (int ks = 0; ks < nk; ++ks) {
+                        const uint64_t bd = make_smem_desc(b0 + ks * 512u, 128, b_sbo);
+#pragma unroll
+                        for (int dz = 0; dz < KZ; ++dz) {
+                            const int zo = zi - dz;
+                            if (zo < zo_a || zo > zo_b) continue;
+                            const int slot = (obase + (zo - zo_a)) % NACC;
                             const int kk = dz * ksz + ks;  // A'' / metadata K step
-                            const uint64_t bd = make_smem_desc(b0 + ks * 512u, 128, b_sbo);
                             const uint32_t ea = tmem + e_col + static_cast<uint32_t>(kk);
                             const uint32_t acc = (dz > 0 || ks > 0) ? 1u : 0u;
                             if constexpr (AT) {

@@ -48,7 +48,7 @@ struct StepParams {
     int32_t nks;               // 32-wide K steps in the A'' image (all slices)
     int32_t patch_w, patch_h, patch_planes;
     int32_t debug_mode;        // ablation bits (profiling only): 1 no stores, 2 no gather, 4 no MMA,
-                               // 8 no right-edge plain stores
+                               // 8 no right-edge plain stores, 16 TMA loads only (3D stream kernel)
     int32_t tmem_cols;         // TMEM allocation (power of two >= the kernel's column budget)
     unsigned long long* trace; // profiling only (sst_plan_set_trace): per CTA {smid, t_start, t_main, t_end}
 };
@@ -156,34 +156,56 @@ __device__ __forceinline__ void tile_offsets(int gw, int patch_w, int32_t (&toff
 }
 
 // One batch of B'': B''[q, tile] = patch[tile_origin + koff[q]] as f16 (RNE), written
-// into the UMMA MN-major operand (8 tiles per 16-byte core-matrix row).
+// into the UMMA MN-major operand (8 tiles per 16-byte core-matrix row). Sweeps are
+// processed UNR at a time: all their shared loads are issued before the first
+// conversion, so the loop is not bound by one LDS round trip per sweep.
+template <int GPW, int UNR>
+__device__ __forceinline__ void gather_sweeps(uint32_t pbase, uint32_t bbase, const int32_t* sGsrc,
+                                              const int32_t* sGdst, int j0, int gw, uint32_t gstride,
+                                              uint32_t lane, const int32_t (&toff)[GPW][8]) {
+    uint32_t src[UNR], dst[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+        src[u] = pbase + static_cast<uint32_t>(sGsrc[(j0 + u) * 32 + lane]);
+        dst[u] = bbase + static_cast<uint32_t>(sGdst[(j0 + u) * 32 + lane]);
+    }
+    float v[UNR][GPW][8];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+#pragma unroll
+        for (int gi = 0; gi < GPW; ++gi)
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[u][gi][t]) : "r"(src[u] + toff[gi][t]));
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+#pragma unroll
+        for (int gi = 0; gi < GPW; ++gi) {
+            uint32_t h[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const __half2 hv = __floats2half2_rn(v[u][gi][2 * i], v[u][gi][2 * i + 1]);
+                h[i] = *reinterpret_cast<const uint32_t*>(&hv);
+            }
+            const uint32_t d = dst[u] + static_cast<uint32_t>(gw + kGatherWarps * gi) * gstride;
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(d), "r"(h[0]), "r"(h[1]), "r"(h[2]),
+                         "r"(h[3])
+                         : "memory");
+        }
+}
+
 template <int GPW>
 __device__ __forceinline__ void gather_batch(uint32_t pbase, uint32_t bbase, const int32_t* sGsrc,
                                              const int32_t* sGdst, int nsweeps, int gw,
                                              uint32_t gstride, uint32_t lane,
                                              const int32_t (&toff)[GPW][8]) {
+    constexpr int UNR = GPW >= 2 ? 2 : 3;  // 24-32 loads in flight per lane
+    int j = 0;
 #pragma unroll 1
-    for (int j = 0; j < nsweeps; ++j) {
-        const uint32_t src = pbase + static_cast<uint32_t>(sGsrc[j * 32 + lane]);
-        const uint32_t dst = bbase + static_cast<uint32_t>(sGdst[j * 32 + lane]);
-#pragma unroll
-        for (int gi = 0; gi < GPW; ++gi) {
-            float v[8];
-#pragma unroll
-            for (int t = 0; t < 8; ++t)
-                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[t]) : "r"(src + toff[gi][t]));
-            uint32_t h[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const __half2 hv = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
-                h[i] = *reinterpret_cast<const uint32_t*>(&hv);
-            }
-            const uint32_t d = dst + static_cast<uint32_t>(gw + kGatherWarps * gi) * gstride;
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(d), "r"(h[0]), "r"(h[1]),
-                         "r"(h[2]), "r"(h[3])
-                         : "memory");
-        }
-    }
+    for (; j + UNR <= nsweeps; j += UNR)
+        gather_sweeps<GPW, UNR>(pbase, bbase, sGsrc, sGdst, j, gw, gstride, lane, toff);
+#pragma unroll 1
+    for (; j < nsweeps; ++j) gather_sweeps<GPW, 1>(pbase, bbase, sGsrc, sGdst, j, gw, gstride, lane, toff);
 }
 
 template <int CW>
