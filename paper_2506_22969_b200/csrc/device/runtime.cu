@@ -190,6 +190,7 @@ struct sst_plan {
     sst_storage storage{};
     int smem = 0, num_sms = 0;
     int tmem_cols = 256;  // TMEM allocation of the chosen variant
+    int zchunk = 0;       // 3D stream kernel unit order (SST_ZCHUNK; 0 = whole columns)
     unsigned long long* trace = nullptr;  // profiling: per-CTA timestamps (sst_plan_set_trace)
     // device constants
     void* d_a = nullptr;
@@ -329,6 +330,7 @@ struct sst_plan {
         p.patch_planes = img.geo.patch_planes;
         p.debug_mode = debug_mode;
         p.tmem_cols = tmem_cols;
+        p.zchunk = zchunk;
         p.trace = trace;
         return p;
     }
@@ -508,6 +510,7 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
                                              origin.data(), d->window_w, d->window_h);
         P->variant->configure(P->smem);
         if (const char* dm = std::getenv("SST_DEBUG_MODE")) P->debug_mode = std::atoi(dm);
+        if (const char* zc = std::getenv("SST_ZCHUNK")) P->zchunk = std::atoi(zc);
 
         P->storage.left_pad = lp;
         P->storage.row_pitch = (lp + static_cast<uint64_t>(P->gx) + aln - 1) / aln * aln;

@@ -28,14 +28,24 @@ __host__ __device__ inline SmemLayout smem_layout_stream(int nks, int k_pad, int
                                     NS, AT);
 }
 
-// Iterates the runs of a CTA's unit range: calls fn(col, zo_a, zo_b) for each run
-// (window-relative output planes, inclusive).
+// Iterates the runs of a CTA's unit range: calls fn(band, zo_a, zo_b) for each run
+// (window-relative output planes, inclusive). Units are ordered z-chunk-major:
+// u = (zc * nby + band) * L + zl for chunks of L = zchunk planes (the last one
+// shorter), so at any time all groups work inside one slab of ~L planes
+// (locality for DRAM pages and L2; the y halo shared by consecutive bands of a
+// group hits in L2), at the cost of 2r re-entry planes per L outputs. zchunk = 0:
+// one chunk (runs are whole columns).
 template <class Fn>
-__device__ __forceinline__ void for_each_run(int u0, int u1, int ozw, Fn&& fn) {
+__device__ __forceinline__ void for_each_run(int u0, int u1, int ozw, int nby, int zchunk, Fn&& fn) {
+    const int L = zchunk > 0 && zchunk < ozw ? zchunk : ozw;
+    const int nzc = (ozw + L - 1) / L;
     for (int u = u0; u < u1;) {
-        const int col = u / ozw, zo_a = u % ozw;
-        const int len = min(u1 - u, ozw - zo_a);
-        fn(col, zo_a, zo_a + len - 1);
+        const int zc = min(u / (nby * L), nzc - 1);
+        const int Lc = zc == nzc - 1 ? ozw - zc * L : L;
+        const int rem = u - nby * L * zc;
+        const int band = rem / Lc, zl = rem % Lc;
+        const int len = min(u1 - u, Lc - zl);
+        fn(band, zc * L + zl, zc * L + zl + len - 1);
         u += len;
     }
 }
@@ -134,12 +144,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         Y0 = by * (TYB * kTileH);
     };
 
-    if (warp == 0) {
+    if (warp == 0 && !(p.debug_mode & 32)) {
         // ------------------------------------------------------ TMA producer
         if (elect_one()) {
             const uint32_t pbytes = static_cast<uint32_t>(p.patch_w * p.patch_h) * 4u;
             int it = 0;
-            for_each_run(u0, u1, ozw, [&](int col, int zo_a, int zo_b) {
+            for_each_run(u0, u1, ozw, p.nby, p.zchunk, [&](int col, int zo_a, int zo_b) {
                 int X0, Y0;
                 col_xy(col, X0, Y0);
                 // input (storage) planes of outputs zo_a..zo_b: zo_a .. zo_b + 2R
@@ -159,13 +169,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (p.debug_mode & 16) {
         // TMA-only ablation: the other roles idle
+    } else if ((p.debug_mode & 32) && warp < kEpiWarp0) {
+        // store-only ablation: only the epilogue runs (writes zeros)
     } else if (warp == 1) {
         // -------------------------------------------------------- MMA issuer
         const uint32_t idesc = make_idesc_f16(128, N, true, 0, 1);
         const uint32_t b_sbo = static_cast<uint32_t>(p.k_pad) * 16u;
         const uint32_t a0 = smem_u32(sA);
         int it = 0, obase = 0;
-        for_each_run(u0, u1, ozw, [&](int col, int zo_a, int zo_b) {
+        for_each_run(u0, u1, ozw, p.nby, p.zchunk, [&](int col, int zo_a, int zo_b) {
             (void)col;
             for (int zi = zo_a; zi <= zo_b + 2 * R; ++zi, ++it) {  // window-relative input plane
                 const int s = it % NB;
@@ -220,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t gstride = static_cast<uint32_t>(p.k_pad) * 16u;
         const int nsweeps = (active && !(p.debug_mode & 2)) ? ksz : 0;
         int it = 0;
-        for_each_run(u0, u1, ozw, [&](int col, int zo_a, int zo_b) {
+        for_each_run(u0, u1, ozw, p.nby, p.zchunk, [&](int col, int zo_a, int zo_b) {
             (void)col;
             for (int zi = zo_a; zi <= zo_b + 2 * R; ++zi, ++it) {
                 const int ps = it % NP, s = it % NB;
@@ -241,20 +253,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t q = static_cast<uint32_t>(warp % 4);
         const int etid = threadIdx.x - kEpiWarp0 * 32;
         int o = 0;
-        for_each_run(u0, u1, ozw, [&](int col, int zo_a, int zo_b) {
+        for_each_run(u0, u1, ozw, p.nby, p.zchunk, [&](int col, int zo_a, int zo_b) {
             int X0, Y0;
             col_xy(col, X0, Y0);
             for (int zo = zo_a; zo <= zo_b; ++zo, ++o) {
                 const int slot = o % NACC;
-                mbar_wait(&d_full[slot], (o / NACC) & 1);
-                tc_fence_after();
                 uint32_t v[NBOX][CW];
-                tmem_load_batch<TYB>(tmem + ((q * 32u) << 16) + static_cast<uint32_t>(slot * N), v);
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&d_empty[slot]);
+                if (p.debug_mode & 32) {
+#pragma unroll
+                    for (int c = 0; c < NBOX; ++c)
+#pragma unroll
+                        for (int i = 0; i < CW; ++i) v[c][i] = 0u;
+                } else {
+                    mbar_wait(&d_full[slot], (o / NACC) & 1);
+                    tc_fence_after();
+                    tmem_load_batch<TYB>(tmem + ((q * 32u) << 16) + static_cast<uint32_t>(slot * N), v);
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&d_empty[slot]);
+                }
                 if (!(p.debug_mode & 1))
-                    store_batch<3, TYB, NS>(p, tmap_out, buf_of(p, p.src ^ 1), v, sS, L.s_stride, o, X0, Y0, p.slow_lo + zo, q,
+                    store_batch<3, TYB, NS, true>(p, tmap_out, buf_of(p, p.src ^ 1), v, sS, L.s_stride, o, X0, Y0, p.slow_lo + zo, q,
                                         lane, etid);
             }
         });

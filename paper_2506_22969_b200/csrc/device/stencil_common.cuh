@@ -48,8 +48,10 @@ struct StepParams {
     int32_t nks;               // 32-wide K steps in the A'' image (all slices)
     int32_t patch_w, patch_h, patch_planes;
     int32_t debug_mode;        // ablation bits (profiling only): 1 no stores, 2 no gather, 4 no MMA,
-                               // 8 no right-edge plain stores, 16 TMA loads only (3D stream kernel)
+                               // 8 no right-edge plain stores, 16 TMA loads only (3D),
+                               // 32 stores only (zeros), 16 TMA loads only (3D stream kernel)
     int32_t tmem_cols;         // TMEM allocation (power of two >= the kernel's column budget)
+    int32_t zchunk;            // 3D stream kernel: output planes per (band, z-chunk) run; 0 = whole column
     unsigned long long* trace; // profiling only (sst_plan_set_trace): per CTA {smid, t_start, t_main, t_end}
 };
 
@@ -242,7 +244,41 @@ __device__ __forceinline__ void tmem_load_batch(uint32_t taddr, uint32_t (&v)[kT
 // TMA clips the innermost dimension at 16-byte granularity, so the store map ends at
 // ox4 = ox & ~3 and the <= 3 interior columns [ox4, ox) are written with plain stores.
 // Called by all 128 epilogue threads; `nb` (batch count) cycles NS buffers.
-template <int DIMS, int TYB, int NS>
+// Right-edge columns [ox4, ox) (<= 3) of a batch: plain stores (TMA clips stores
+// in 16-byte units). A thread owns x = X0 + 32c + 16 par + dxl, so at most one
+// (c, par) of the batch falls in [ox4, ox) for it; only that branch runs (TYB stores).
+template <int DIMS, int TYB>
+__device__ __forceinline__ void store_right_edge(const StepParams& p, float* dst,
+                                                 const uint32_t (&v)[kTXB / 2][2 * TYB], int X0, int Y0,
+                                                 int Z0, uint32_t q, uint32_t lane) {
+    constexpr int NBOX = kTXB / 2;
+    const int ox = p.gx - 2 * p.r, ox4 = ox & ~3;
+    if (X0 + kTXB * kTileW <= ox4 || (p.debug_mode & 8)) return;
+    const int dxl = static_cast<int>(q) * 4 + static_cast<int>(lane / 8);
+    const int y_lim = DIMS == 2 ? p.slow_hi : p.y_end;
+    const int y0 = Y0 + static_cast<int>(lane % 8);
+    float* rowp = dst + (DIMS == 3 ? static_cast<int64_t>(Z0 + p.r) * p.plane_pitch : 0) +
+                  static_cast<int64_t>(y0 + p.r) * p.row_pitch + p.left_pad + p.r + X0 + dxl;
+    const int64_t ystep = static_cast<int64_t>(kTileH) * p.row_pitch;
+#pragma unroll
+    for (int c = 0; c < NBOX; ++c)
+#pragma unroll
+        for (int par = 0; par < 2; ++par) {
+            const int xo = c * kBoxW + par * kTileW;
+            const int xr = X0 + xo + dxl;
+            if (xr >= ox4 && xr < ox) {
+#pragma unroll
+                for (int ty = 0; ty < TYB; ++ty)
+                    if (y0 + ty * kTileH < y_lim) rowp[xo + ty * ystep] = __uint_as_float(v[c][2 * ty + par]);
+            }
+        }
+}
+
+// EDGE_LATE: issue the right-edge plain stores after the TMA store instead of before
+// the staging barriers (the 3D kernel, which has no cross-CTA flags). The 2D
+// multi-step kernel keeps them early so that its progress flags, published after
+// this batch's barriers, also cover them.
+template <int DIMS, int TYB, int NS, bool EDGE_LATE = false>
 __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorMap* tmap_out, float* dst,
                                             const uint32_t (&v)[kTXB / 2][2 * TYB], uint8_t* sS,
                                             uint32_t s_stride, int nb, int X0, int Y0, int Z0,
@@ -251,31 +287,7 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
     constexpr int CW = 2 * TYB, NBOX = kTXB / 2;
     const uint32_t dy = lane % 8, w4 = (lane / 8) * 4;
     const int ox = p.gx - 2 * p.r, ox4 = ox & ~3;
-    // right-edge columns [ox4, ox) (<= 3): plain stores. A thread owns
-    // x = X0 + 32c + 16 par + dxl, so at most one (c, par) of the batch falls in
-    // [ox4, ox) for it; only that branch runs (TYB stores). They precede the
-    // staging barriers below, so a flag published after this batch's TMA stores
-    // complete also covers them.
-    if (X0 + kTXB * kTileW > ox4 && !(p.debug_mode & 8)) {
-        const int dxl = static_cast<int>(q) * 4 + static_cast<int>(lane / 8);
-        const int y_lim = DIMS == 2 ? p.slow_hi : p.y_end;
-        const int y0 = Y0 + static_cast<int>(dy);
-        float* rowp = dst + (DIMS == 3 ? static_cast<int64_t>(Z0 + p.r) * p.plane_pitch : 0) +
-                      static_cast<int64_t>(y0 + p.r) * p.row_pitch + p.left_pad + p.r + X0 + dxl;
-        const int64_t ystep = static_cast<int64_t>(kTileH) * p.row_pitch;
-#pragma unroll
-        for (int c = 0; c < NBOX; ++c)
-#pragma unroll
-            for (int par = 0; par < 2; ++par) {
-                const int xo = c * kBoxW + par * kTileW;
-                const int xr = X0 + xo + dxl;
-                if (xr >= ox4 && xr < ox) {
-#pragma unroll
-                    for (int ty = 0; ty < TYB; ++ty)
-                        if (y0 + ty * kTileH < y_lim) rowp[xo + ty * ystep] = __uint_as_float(v[c][2 * ty + par]);
-                }
-            }
-    }
+    if constexpr (!EDGE_LATE) store_right_edge<DIMS, TYB>(p, dst, v, X0, Y0, Z0, q, lane);
     const uint32_t buf = static_cast<uint32_t>(nb % NS) * NBOX * s_stride;
     const uint32_t stage = smem_u32(sS) + buf;
     if (etid == 0) bulk_wait_read<NS - 1>();  // this buffer's previous stores have read it
@@ -306,6 +318,7 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
         }
         bulk_commit();
     }
+    if constexpr (EDGE_LATE) store_right_edge<DIMS, TYB>(p, dst, v, X0, Y0, Z0, q, lane);
 }
 
 }  // namespace sst

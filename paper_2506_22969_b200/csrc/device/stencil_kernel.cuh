@@ -195,7 +195,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     const bool multi = p.nsteps > 1;
 
-    if (warp == 0) {
+    if ((p.debug_mode & 32) && warp < kEpiWarp0) {
+        // store-only ablation: only the epilogue runs (writes zeros)
+    } else if (warp == 0) {
         // ------------------------------------------------------ TMA producer
         // (the whole warp walks the loop: lane 0 issues, all lanes refresh counters)
         const uint32_t pbytes = static_cast<uint32_t>(p.patch_w * p.patch_h * p.patch_planes) * 4u;
@@ -333,23 +335,30 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int s = r & 1;
             const uint32_t ph = (r >> 1) & 1;
             ++r;
-            if (multi && etid == 0) {
-                const unsigned long long t0 = global_ns();
-                while (!mbar_try_wait(&d_full[s], ph)) {
-                    if (published < committed && global_ns() - t0 > 2000ull) {
-                        bulk_wait<0>();
-                        publish(committed);
-                    }
-                }
-            } else {
-                mbar_wait(&d_full[s], ph);
-            }
-            tc_fence_after();
             uint32_t v[NBOX][CW];
-            tmem_load_batch<TYB>(tmem + ((q * 32u) << 16) + static_cast<uint32_t>(s * N), v);
-            tc_fence_before();  // accumulator read: hand it back to the MMA warp
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&d_empty[s]);
+            if (p.debug_mode & 32) {  // store-only ablation
+#pragma unroll
+                for (int c = 0; c < NBOX; ++c)
+#pragma unroll
+                    for (int i = 0; i < CW; ++i) v[c][i] = 0u;
+            } else {
+                if (multi && etid == 0) {
+                    const unsigned long long t0 = global_ns();
+                    while (!mbar_try_wait(&d_full[s], ph)) {
+                        if (published < committed && global_ns() - t0 > 2000ull) {
+                            bulk_wait<0>();
+                            publish(committed);
+                        }
+                    }
+                } else {
+                    mbar_wait(&d_full[s], ph);
+                }
+                tc_fence_after();
+                tmem_load_batch<TYB>(tmem + ((q * 32u) << 16) + static_cast<uint32_t>(s * N), v);
+                tc_fence_before();  // accumulator read: hand it back to the MMA warp
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&d_empty[s]);
+            }
             if (!(p.debug_mode & 1))
                 store_batch<DIMS, TYB, kStageBufs>(p, &maps.out[(p.src + t + 1) & 1], buf_of(p, p.src + t + 1),
                                                    v, sS, L.s_stride, r - 1, X0, Y0, Z0, q, lane, etid);
