@@ -304,9 +304,13 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
                          "r"(v[c][i])
                          : "memory");
         }
-    fence_proxy_async_smem();
+    // The named barrier drains every epilogue thread's staging stores (bar.sync has
+    // CTA memory-ordering semantics); the issuing thread then orders them before its
+    // async-proxy (TMA) reads with one proxy fence. A per-thread fence right after the
+    // stores instead costs each thread a MEMBAR over its 32-64 stores in flight.
     named_bar_sync(kEpiBarrier, kEpiWarps * 32);
     if (etid == 0) {
+        fence_proxy_async_smem();
 #pragma unroll
         for (int c = 0; c < NBOX; ++c) {
             const int bx0 = X0 + c * kBoxW;
