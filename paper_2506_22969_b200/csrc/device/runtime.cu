@@ -279,12 +279,20 @@ struct sst_plan {
             // inner extent ends on the last 16-byte boundary of the interior (TMA
             // clips the innermost dimension in 16-byte units); the kernel writes
             // the <= 3 remaining columns directly
-            const cuuint64_t odim[3] = {static_cast<cuuint64_t>(std::max((gx - 2 * r) & ~3, 4)),
+            // the 3D stream kernel also stores the last 16-byte chunk [ox4, ox4 + 4),
+            // staging its ring / pad cells with their current values (kEdgeRing)
+            const int ox = gx - 2 * r;
+            const int oxs = (variant && variant->kz > 0 && (ox & 3)) ? (ox & ~3) + 4 : (ox & ~3);
+            const cuuint64_t odim[3] = {static_cast<cuuint64_t>(std::max(oxs, 4)),
                                         static_cast<cuuint64_t>(dims == 2 ? std::max(hi - lo, 1) : gy - 2 * r),
                                         static_cast<cuuint64_t>(gz - 2 * r)};
             const cuuint32_t obox[3] = {static_cast<cuuint32_t>(sst::kBoxW),
                                         static_cast<cuuint32_t>(tiles_y * sst::kTileH), 1u};
             encode(&maps.out[i], dims, base, odim, gstride, obox, CU_TENSOR_MAP_SWIZZLE_128B);
+            if (dims == 3) {  // right-edge ring chunk loads of the 3D stream kernel
+                const cuuint32_t rbox[3] = {4u, static_cast<cuuint32_t>(tiles_y * sst::kTileH), 1u};
+                encode(&maps.ring[i], 3, buf[i], gdim, gstride, rbox, CU_TENSOR_MAP_SWIZZLE_NONE);
+            }
         }
         map_lo = lo;
         map_hi = hi;
@@ -424,11 +432,13 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
             throw std::invalid_argument("grid smaller than kernel");
 
         // storage: the first interior column (r) of every row lands on a 16-byte
-        // boundary (TMA store requirement). SST_ALIGN=128 aligns it to whole L2 lines
-        // instead (measured slower on 8192^2 Box-2D9P: the patch loads then start
-        // mid-line; kept as an experiment switch)
+        // boundary (TMA store requirement) in 2D. 3D: rows start on 128-byte lines (the z-streaming kernel's TMA stores then
+        // write whole 32-byte sectors only; with its ring-chunk store the row ends
+        // are whole sectors too. Measured: Box-3D27P 512^3 204 -> 196 us). 2D: 16 B.
+        // SST_ALIGN=16|128 overrides (experiments).
         const char* al = std::getenv("SST_ALIGN");
-        const uint64_t aln = (al && std::atoi(al) == 128) ? 32 : 4;  // elements
+        const int al_bytes = al ? std::atoi(al) : (d->dims == 3 ? 128 : 16);
+        const uint64_t aln = al_bytes == 128 ? 32 : 4;  // elements
         const uint64_t lp = (aln - static_cast<uint64_t>(P->r) % aln) % aln;
         P->load_x0 = static_cast<int>(lp & ~uint64_t{3});  // 16-byte aligned patch start
         int max_smem = 0;
@@ -514,6 +524,11 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
 
         P->storage.left_pad = lp;
         P->storage.row_pitch = (lp + static_cast<uint64_t>(P->gx) + aln - 1) / aln * aln;
+        {  // room for the 3D stream kernel's full last 16-byte store chunk
+            const uint64_t ox = static_cast<uint64_t>(P->gx - 2 * P->r);
+            const uint64_t need = lp + static_cast<uint64_t>(P->r) + (ox + 3) / 4 * 4;
+            if (P->storage.row_pitch < need) P->storage.row_pitch = (need + aln - 1) / aln * aln;
+        }
         P->storage.plane_pitch = P->storage.row_pitch * static_cast<uint64_t>(P->gy);
         P->storage.bytes = P->storage.plane_pitch * static_cast<uint64_t>(P->gz) * 4;
 

@@ -22,10 +22,21 @@
 
 namespace sst {
 
+// Right-edge ring cache (see kEdgeRing in stencil_common.cuh): one slot per
+// gathered input plane, kRingSlots deep. Slot reuse is safe by pipeline depth: the
+// gather of plane it + kRingSlots waits (b_empty) for the MMA of plane
+// it + kRingSlots - NB, which waited (d_empty) for the epilogue to drain output
+// it + kRingSlots - NB - NACC - R > it - R, the last reader of slot it.
+constexpr int kRingSlots = 16;
+
 template <int TYB, int NP, int KZ, int NB, int NACC, int NS, bool AT>
 __host__ __device__ inline SmemLayout smem_layout_stream(int nks, int k_pad, int patch_w, int patch_h) {
-    return smem_layout_generic<TYB>(nks, k_pad, patch_w, patch_h, 1, NP, NB, 2 * NP + 2 * NB + 2 * NACC,
-                                    NS, AT);
+    static_assert(kRingSlots > NB + NACC + (KZ - 1) / 2, "ring cache slots vs pipeline depth");
+    SmemLayout L = smem_layout_generic<TYB>(nks, k_pad, patch_w, patch_h, 1, NP, NB,
+                                            2 * NP + 2 * NB + 2 * NACC + kRingSlots, NS, AT);
+    L.ring = align_up(L.total, 16);
+    L.total = align_up(L.ring + static_cast<uint32_t>(kRingSlots * TYB * kTileH * 4 * 4), 128);
+    return L;
 }
 
 // Iterates the runs of a CTA's unit range: calls fn(band, zo_a, zo_b) for each run
@@ -82,6 +93,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* b_empty = b_full + NB;
     uint64_t* d_full = b_full + 2 * NB;
     uint64_t* d_empty = d_full + NACC;
+    uint64_t* ring_full = d_empty + NACC;  // [kRingSlots]
+    float* sRing = reinterpret_cast<float*>(smem + L.ring);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem_slot);
 
     const int warp = threadIdx.x / 32;
@@ -102,9 +115,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&d_full[s], 1);
             mbar_init(&d_empty[s], kEpiWarps);
         }
+        for (int s = 0; s < kRingSlots; ++s) mbar_init(&ring_full[s], 1);
         fence_mbar_init();
         tma_prefetch_desc(&maps.in[p.src]);
         tma_prefetch_desc(&maps.out[p.src ^ 1]);
+        tma_prefetch_desc(&maps.ring[p.src]);
     }
     if (warp == 1) tmem_alloc(tmem_slot, static_cast<uint32_t>(p.tmem_cols));
     stage_constants<AT>(p, sA, sB, sGsrc, sGdst);
@@ -148,6 +163,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------------ TMA producer
         if (elect_one()) {
             const uint32_t pbytes = static_cast<uint32_t>(p.patch_w * p.patch_h) * 4u;
+            const int ox = p.gx - 2 * p.r, ox4 = ox & ~3;
+            const bool edge = ox4 != ox && bx * (kTXB * kTileW) + kTXB * kTileW > ox && !(p.debug_mode & 24);
             int it = 0;
             for_each_run(u0, u1, ozw, p.nby, p.zchunk, [&](int col, int zo_a, int zo_b) {
                 int X0, Y0;
@@ -162,6 +179,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     mbar_arrive_expect_tx(&patch_full[s], pbytes);
                     tma_load_3d(sP + s * L.p_stride, tmap_in, &patch_full[s], X0 + p.load_x0, Y0, z);
+                    if (edge) {  // right-edge chunk [ox4, ox4 + 4) of the TYB*8 output rows
+                        const int rs = it % kRingSlots;
+                        mbar_arrive_expect_tx(&ring_full[rs], static_cast<uint32_t>(TYB * kTileH * 4 * 4));
+                        tma_load_3d(sRing + rs * (TYB * kTileH * 4), &maps.ring[p.src], &ring_full[rs],
+                                    static_cast<int>(p.left_pad) + p.r + ox4, Y0 + p.r, z);
+                    }
                 }
             });
             if (p.debug_mode & 16)
@@ -240,19 +263,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&b_empty[s], ((it / NB) & 1) ^ 1);
                 gather_batch<GPW>(smem_u32(sP + ps * L.p_stride), smem_u32(sB + s * L.b_stride),
                                   sGsrc, sGdst, nsweeps, gw, gstride, lane, toff);
+
                 fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(&b_full[s]);
-                    mbar_arrive(&patch_empty[ps]);
-                }
+                if (lane == 0) mbar_arrive(&b_full[s]);
+                if (lane == 0) mbar_arrive(&patch_empty[ps]);
             }
         });
     } else {
         // ---------------------------------------------------------- epilogue
         const uint32_t q = static_cast<uint32_t>(warp % 4);
         const int etid = threadIdx.x - kEpiWarp0 * 32;
-        int o = 0;
+        int o = 0, it_base = 0;  // it_base: gather iteration of the run's first input plane
+        const int ox = p.gx - 2 * p.r;
+        const bool edge = (ox & 3) != 0 && bx * (kTXB * kTileW) + kTXB * kTileW > ox && !(p.debug_mode & 24);
         for_each_run(u0, u1, ozw, p.nby, p.zchunk, [&](int col, int zo_a, int zo_b) {
             int X0, Y0;
             col_xy(col, X0, Y0);
@@ -272,10 +296,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&d_empty[slot]);
                 }
+                const float* ring = nullptr;
+                if (edge && !(p.debug_mode & 32)) {  // center input plane of output zo
+                    const int ci = it_base + (zo - zo_a) + R;
+                    mbar_wait(&ring_full[ci % kRingSlots], (ci / kRingSlots) & 1);
+                    ring = sRing + (ci % kRingSlots) * (TYB * kTileH * 4);
+                }
                 if (!(p.debug_mode & 1))
-                    store_batch<3, TYB, NS, true>(p, tmap_out, buf_of(p, p.src ^ 1), v, sS, L.s_stride, o, X0, Y0, p.slow_lo + zo, q,
-                                        lane, etid);
+                    store_batch<3, TYB, NS, kEdgeRing>(p, tmap_out, buf_of(p, p.src ^ 1), v, sS, L.s_stride, o, X0,
+                                                       Y0, p.slow_lo + zo, q, lane, etid, ring);
             }
+            it_base += zo_b - zo_a + 1 + 2 * R;
         });
         if (etid == 0) bulk_wait<0>();
     }

@@ -24,6 +24,7 @@ constexpr int kStageBufs = 1;           // batch staging buffers (TMA stores in 
 struct MapSet {
     CUtensorMap in[2];
     CUtensorMap out[2];
+    CUtensorMap ring[2];  // 3D stream kernel: {4, TYB*8, 1} boxes of the right-edge chunk (kEdgeRing)
 };
 
 struct StepParams {
@@ -274,20 +275,48 @@ __device__ __forceinline__ void store_right_edge(const StepParams& p, float* dst
         }
 }
 
-// EDGE_LATE: issue the right-edge plain stores after the TMA store instead of before
-// the staging barriers (the 3D kernel, which has no cross-CTA flags). The 2D
-// multi-step kernel keeps them early so that its progress flags, published after
-// this batch's barriers, also cover them.
-template <int DIMS, int TYB, int NS, bool EDGE_LATE = false>
+// Right-edge handling of store_batch:
+//   kEdgePlain  the <= 3 columns [ox4, ox) as plain stores, before the staging
+//               barriers (the 2D multi-step kernel's progress flags must cover them)
+//   kEdgeRing   no plain stores: the store map runs to ox4 + 4 and the cells
+//               [ox, ox4 + 4) of that last 16-byte chunk (boundary ring / row pad,
+//               constant in time and equal in both buffers) are staged with their
+//               current values, which the producer loaded (one small TMA box per
+//               input plane) into `ring` (TYB*8 rows x 4 floats). Scattered 4-byte
+//               stores on every plane of the right-edge CTAs cost the 3D kernel ~5 %
+//               (and leave partially written 32-byte sectors behind).
+enum EdgeMode { kEdgePlain = 0, kEdgeRing = 1 };
+
+template <int DIMS, int TYB, int NS, int EDGE = kEdgePlain>
 __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorMap* tmap_out, float* dst,
-                                            const uint32_t (&v)[kTXB / 2][2 * TYB], uint8_t* sS,
+                                            uint32_t (&v)[kTXB / 2][2 * TYB], uint8_t* sS,
                                             uint32_t s_stride, int nb, int X0, int Y0, int Z0,
-                                            uint32_t q, uint32_t lane, int etid) {
+                                            uint32_t q, uint32_t lane, int etid, const float* ring = nullptr) {
     using namespace ptx;
     constexpr int CW = 2 * TYB, NBOX = kTXB / 2;
     const uint32_t dy = lane % 8, w4 = (lane / 8) * 4;
     const int ox = p.gx - 2 * p.r, ox4 = ox & ~3;
-    if constexpr (!EDGE_LATE) store_right_edge<DIMS, TYB>(p, dst, v, X0, Y0, Z0, q, lane);
+    // last column the store map covers (exclusive)
+    const int oxs = (EDGE == kEdgeRing && ox4 != ox) ? ox4 + 4 : ox4;
+    if constexpr (EDGE == kEdgePlain) {
+        store_right_edge<DIMS, TYB>(p, dst, v, X0, Y0, Z0, q, lane);
+    } else {
+        if (ring != nullptr && X0 + kTXB * kTileW > ox) {
+            const int dxl = static_cast<int>(q) * 4 + static_cast<int>(lane / 8);
+#pragma unroll
+            for (int c = 0; c < NBOX; ++c)
+#pragma unroll
+                for (int par = 0; par < 2; ++par) {
+                    const int xr = X0 + c * kBoxW + par * kTileW + dxl;
+                    if (xr >= ox && xr < oxs) {
+#pragma unroll
+                        for (int ty = 0; ty < TYB; ++ty)
+                            v[c][2 * ty + par] =
+                                __float_as_uint(ring[(ty * kTileH + static_cast<int>(dy)) * 4 + (xr - ox4)]);
+                    }
+                }
+        }
+    }
     const uint32_t buf = static_cast<uint32_t>(nb % NS) * NBOX * s_stride;
     const uint32_t stage = smem_u32(sS) + buf;
     if (etid == 0) bulk_wait_read<NS - 1>();  // this buffer's previous stores have read it
@@ -314,7 +343,7 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
 #pragma unroll
         for (int c = 0; c < NBOX; ++c) {
             const int bx0 = X0 + c * kBoxW;
-            if (bx0 >= ox4) break;  // fully clipped
+            if (bx0 >= oxs) break;  // fully clipped
             if (DIMS == 2)
                 tma_store_2d(tmap_out, sS + buf + c * s_stride, bx0, Y0 - p.slow_lo);  // map starts at the window
             else
@@ -322,7 +351,6 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
         }
         bulk_commit();
     }
-    if constexpr (EDGE_LATE) store_right_edge<DIMS, TYB>(p, dst, v, X0, Y0, Z0, q, lane);
 }
 
 }  // namespace sst
