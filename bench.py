@@ -203,7 +203,8 @@ def run_engine(args, cfg, cfg_name):
     # weak scaling: each rank owns a slab of `dims` rows (plus halo rows)
     from paper_2506_22969_b200.multigpu import SlabStencil
 
-    eng = SlabStencil(stencil, dims, rank=rank, world=ws, device=local, fuse=args.fuse)
+    eng = SlabStencil(stencil, dims, rank=rank, world=ws, device=local, fuse=args.fuse,
+                      precision=args.precision)
     grid = eng.make_local_input(seed=1)  # dense fp32 torch tensor on the device
     eng.load(grid)
     stream = torch.cuda.current_stream(dev)
@@ -267,7 +268,7 @@ def run_engine(args, cfg, cfg_name):
     alg_bytes = 8.0 * interior
     peak, peak_kind = _peaks()
     achieved = alg_bytes / t_kernel / 1e9
-    traffic = _load_traffic(cfg_name if args.fuse == 1 else f"{cfg_name}_fuse{args.fuse}")
+    traffic = _load_traffic(cfg_name if args.fuse == 1 and args.precision == "f16" else None)
 
     # e2e through the public API from host memory (rank-local slab)
     e2e = None
@@ -345,6 +346,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--precision", default="f16", choices=["f16", "f16x2"],
+                    help="operand precision: f16 (round16 operands) or f16x2 (split hi+lo operand, ~fp32)")
     ap.add_argument("--fuse", type=int, default=1,
                     help="temporal fusion factor (reference fuse_time_steps); steps count original time steps")
     args = ap.parse_args()

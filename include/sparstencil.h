@@ -53,8 +53,13 @@ typedef enum sst_status {
     SST_ERR_NO_DEVICE = 6
 } sst_status;
 
-/* operand precision of the tensor-core path (storage is always fp32) */
-enum { SST_PREC_F16 = 1 };
+/* operand precision of the tensor-core path (storage is always fp32):
+ *   SST_PREC_F16    B'' operand rounded to binary16 (RNE: the reference's round16
+ *                   operand semantics), f32 accumulation
+ *   SST_PREC_F16X2  B'' split into hi + lo binary16 terms (the MMA sees [A'' A''] x
+ *                   [B_hi; B_lo], twice the K): ~fp32-accurate steps; needs A''
+ *                   weights exact in binary16 (all presets are) */
+enum { SST_PREC_F16 = 1, SST_PREC_F16X2 = 2 };
 
 /* ---------------------------------------------------------------- compile */
 
@@ -106,7 +111,7 @@ typedef struct sst_plan_desc {
     const uint8_t* a_meta;    /* rows x cols/4 bytes pos0 | pos1 << 2 */
     const uint64_t* col_origin; /* cols entries, UINT64_MAX = zero column */
     uint64_t window_w, window_h, window_d;
-    int32_t precision;        /* SST_PREC_F16 */
+    int32_t precision;        /* SST_PREC_F16 or SST_PREC_F16X2 */
     uint32_t fuse;            /* time steps per operator application (fuse_time_steps); 0 = 1 */
 } sst_plan_desc;
 

@@ -14,6 +14,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libsparstencil.so"
 
 SST_OK = 0
 SST_PREC_F16 = 1
+SST_PREC_F16X2 = 2
 
 # every symbol include/sparstencil.h declares (checked by tests/test_capi.py)
 EXPORTED = [

@@ -339,6 +339,7 @@ struct sst_plan {
         p.debug_mode = debug_mode;
         p.tmem_cols = tmem_cols;
         p.zchunk = zchunk;
+        p.lo_sweep0 = img.lo_sweep0;
         p.trace = trace;
         return p;
     }
@@ -409,7 +410,9 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
     try {
         if (!d || !out) throw std::invalid_argument("null argument");
         *out = nullptr;
-        if (d->precision != SST_PREC_F16) throw std::invalid_argument("unsupported precision");
+        if (d->precision != SST_PREC_F16 && d->precision != SST_PREC_F16X2)
+            throw std::invalid_argument("unsupported precision");
+        const int terms = d->precision == SST_PREC_F16X2 ? 2 : 1;
         if (d->dims != 2 && d->dims != 3)
             throw std::invalid_argument("device path supports 2D and 3D stencils (m' = 128 needs r2 > 1)");
         if (d->r1 != sst::kTileW || d->r2 != sst::kTileH || d->rows != 128)
@@ -446,11 +449,12 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
            "cudaDeviceGetAttribute");
         ck(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, device),
            "cudaDeviceGetAttribute");
-        const int k_pad = static_cast<int>((d->cols + 31) / 32 * 32);
+        const int k_pad = static_cast<int>((d->cols + 31) / 32 * 32) * terms;
         stensor::BatchGeometry geo;
         geo.dims = d->dims;
         geo.k = d->k;
         geo.tiles_x = 8;
+        geo.terms = terms;
         geo.patch_planes = d->dims == 3 ? d->k : 1;
         // the patch is loaded from the 16-byte aligned storage column X0 + load_x0,
         // lp & 3 cells left of the window origin (TMA box starts must be aligned)

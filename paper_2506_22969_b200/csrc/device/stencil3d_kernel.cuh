@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&patch_full[ps], (it / NP) & 1);
                 mbar_wait(&b_empty[s], ((it / NB) & 1) ^ 1);
                 gather_batch<GPW>(smem_u32(sP + ps * L.p_stride), smem_u32(sB + s * L.b_stride),
-                                  sGsrc, sGdst, nsweeps, gw, gstride, lane, toff);
+                                  sGsrc, sGdst, nsweeps, gw, gstride, lane, toff, p.lo_sweep0);
 
                 fence_proxy_async_smem();
                 __syncwarp();

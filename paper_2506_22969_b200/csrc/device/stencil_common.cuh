@@ -53,6 +53,7 @@ struct StepParams {
                                // 32 stores only (zeros), 16 TMA loads only (3D stream kernel)
     int32_t tmem_cols;         // TMEM allocation (power of two >= the kernel's column budget)
     int32_t zchunk;            // 3D stream kernel: output planes per (band, z-chunk) run; 0 = whole column
+    int32_t lo_sweep0;         // first gather sweep writing B_lo rows (SST_PREC_F16X2); = k_pad/32 otherwise
     unsigned long long* trace; // profiling only (sst_plan_set_trace): per CTA {smid, t_start, t_main, t_end}
 };
 
@@ -162,7 +163,9 @@ __device__ __forceinline__ void tile_offsets(int gw, int patch_w, int32_t (&toff
 // into the UMMA MN-major operand (8 tiles per 16-byte core-matrix row). Sweeps are
 // processed UNR at a time: all their shared loads are issued before the first
 // conversion, so the loop is not bound by one LDS round trip per sweep.
-template <int GPW, int UNR>
+// LO: the sweep writes the low term of the split operand, f16(v - f16(v)) (exact
+// residual in f32; B_hi + B_lo carries ~22 significant bits of v).
+template <int GPW, int UNR, bool LO = false>
 __device__ __forceinline__ void gather_sweeps(uint32_t pbase, uint32_t bbase, const int32_t* sGsrc,
                                               const int32_t* sGdst, int j0, int gw, uint32_t gstride,
                                               uint32_t lane, const int32_t (&toff)[GPW][8]) {
@@ -187,7 +190,12 @@ __device__ __forceinline__ void gather_sweeps(uint32_t pbase, uint32_t bbase, co
             uint32_t h[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const __half2 hv = __floats2half2_rn(v[u][gi][2 * i], v[u][gi][2 * i + 1]);
+                float a = v[u][gi][2 * i], b = v[u][gi][2 * i + 1];
+                if constexpr (LO) {
+                    a -= __half2float(__float2half_rn(a));
+                    b -= __half2float(__float2half_rn(b));
+                }
+                const __half2 hv = __floats2half2_rn(a, b);
                 h[i] = *reinterpret_cast<const uint32_t*>(&hv);
             }
             const uint32_t d = dst[u] + static_cast<uint32_t>(gw + kGatherWarps * gi) * gstride;
@@ -197,18 +205,28 @@ __device__ __forceinline__ void gather_sweeps(uint32_t pbase, uint32_t bbase, co
         }
 }
 
+template <int GPW, bool LO>
+__device__ __forceinline__ void gather_range(uint32_t pbase, uint32_t bbase, const int32_t* sGsrc,
+                                             const int32_t* sGdst, int j, int j_end, int gw, uint32_t gstride,
+                                             uint32_t lane, const int32_t (&toff)[GPW][8]) {
+    constexpr int UNR = GPW >= 2 ? 2 : 3;  // 24-32 loads in flight per lane
+#pragma unroll 1
+    for (; j + UNR <= j_end; j += UNR)
+        gather_sweeps<GPW, UNR, LO>(pbase, bbase, sGsrc, sGdst, j, gw, gstride, lane, toff);
+#pragma unroll 1
+    for (; j < j_end; ++j) gather_sweeps<GPW, 1, LO>(pbase, bbase, sGsrc, sGdst, j, gw, gstride, lane, toff);
+}
+
+// Sweeps [0, lo0) write B'' (or B_hi), sweeps [lo0, nsweeps) B_lo (SST_PREC_F16X2).
 template <int GPW>
 __device__ __forceinline__ void gather_batch(uint32_t pbase, uint32_t bbase, const int32_t* sGsrc,
                                              const int32_t* sGdst, int nsweeps, int gw,
                                              uint32_t gstride, uint32_t lane,
-                                             const int32_t (&toff)[GPW][8]) {
-    constexpr int UNR = GPW >= 2 ? 2 : 3;  // 24-32 loads in flight per lane
-    int j = 0;
-#pragma unroll 1
-    for (; j + UNR <= nsweeps; j += UNR)
-        gather_sweeps<GPW, UNR>(pbase, bbase, sGsrc, sGdst, j, gw, gstride, lane, toff);
-#pragma unroll 1
-    for (; j < nsweeps; ++j) gather_sweeps<GPW, 1>(pbase, bbase, sGsrc, sGdst, j, gw, gstride, lane, toff);
+                                             const int32_t (&toff)[GPW][8], int lo0) {
+    const int hi_end = min(nsweeps, lo0);
+    gather_range<GPW, false>(pbase, bbase, sGsrc, sGdst, 0, hi_end, gw, gstride, lane, toff);
+    if (hi_end < nsweeps)
+        gather_range<GPW, true>(pbase, bbase, sGsrc, sGdst, hi_end, nsweeps, gw, gstride, lane, toff);
 }
 
 template <int CW>

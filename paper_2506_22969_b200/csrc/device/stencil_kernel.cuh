@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&patch_full[ps], pph);
             mbar_wait(&b_empty[s], ph ^ 1);
             gather_batch<GPW>(smem_u32(sP + ps * L.p_stride), smem_u32(sB + s * L.b_stride), sGsrc,
-                              sGdst, nsweeps, gw, gstride, lane, toff);
+                              sGdst, nsweeps, gw, gstride, lane, toff, p.lo_sweep0);
             fence_proxy_async_smem();  // generic-proxy writes -> tensor-core reads
             __syncwarp();
             if (lane == 0) {

@@ -47,6 +47,13 @@ std::uint16_t f32_to_f16_bits(float f) {
     return static_cast<std::uint16_t>(sign | (h - (112u << 10)));
 }
 
+double f16_bits_to_double(std::uint16_t h) {
+    const int e = (h >> 10) & 0x1f, m = h & 0x3ff;
+    const double v = e == 0 ? std::ldexp(static_cast<double>(m), -24)
+                            : std::ldexp(static_cast<double>(m | 0x400), e - 25);
+    return (h & 0x8000) ? -v : v;
+}
+
 namespace {
 
 // distinct addresses per bank among the 32 lanes of one gather LDS
@@ -178,6 +185,39 @@ DeviceImage build_device_image(const BatchGeometry& geo_in, std::size_t rows, st
             img.gather_src[j * 32 + lane] = img.koff[k] * 4;
             img.gather_dst[j * 32 + lane] = static_cast<std::int32_t>(k) * 16;
         }
+    img.lo_sweep0 = static_cast<int>(k_pad / 32);
+    if (g.terms == 2) {
+        // split operand: every z slice's K becomes [K rows -> B_hi; K rows -> B_lo]
+        // and A'' (with its metadata) is repeated for the second half, so the MMA
+        // accumulates A'' B_hi + A'' B_lo. Exact only if A'' itself is binary16.
+        for (std::size_t i = 0; i < rows * half_cols; ++i) {
+            const double v = values[i];
+            if (f16_bits_to_double(f32_to_f16_bits(static_cast<float>(v))) != v)
+                throw std::invalid_argument("f16x2 needs A'' weights exact in binary16 (use f16)");
+        }
+        std::vector<std::uint16_t> a2(2 * img.a_smem.size());
+        std::vector<std::uint32_t> e2(2 * img.e_words.size());
+        for (std::size_t dz = 0; dz < nsl; ++dz)
+            for (std::size_t t = 0; t < 2 * ksteps; ++t) {
+                const std::size_t from = dz * ksteps + t % ksteps, to = dz * 2 * ksteps + t;
+                std::copy_n(img.a_smem.begin() + static_cast<std::ptrdiff_t>(from * 2048), 2048,
+                            a2.begin() + static_cast<std::ptrdiff_t>(to * 2048));
+                std::copy_n(img.e_words.begin() + static_cast<std::ptrdiff_t>(from * 128), 128,
+                            e2.begin() + static_cast<std::ptrdiff_t>(to * 128));
+            }
+        img.a_smem = std::move(a2);
+        img.e_words = std::move(e2);
+        const std::size_t sweeps = k_pad / 32;
+        img.koff.resize(2 * k_pad);
+        std::copy_n(img.koff.begin(), k_pad, img.koff.begin() + static_cast<std::ptrdiff_t>(k_pad));
+        img.gather_src.resize(2 * sweeps * 32);
+        img.gather_dst.resize(2 * sweeps * 32);
+        for (std::size_t i = 0; i < sweeps * 32; ++i) {
+            img.gather_src[sweeps * 32 + i] = img.gather_src[i];
+            img.gather_dst[sweeps * 32 + i] = img.gather_dst[i] + static_cast<std::int32_t>(k_pad) * 16;
+        }
+        g.k_pad = static_cast<int>(2 * k_pad);
+    }
     return img;
 }
 

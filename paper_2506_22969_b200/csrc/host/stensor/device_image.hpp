@@ -22,6 +22,7 @@ struct BatchGeometry {
     int patch_planes = 1;      // kz (3D) or 1
     int k_pad = 0;             // logical K rounded to the MMA K step (32)
     int z_slices = 1;          // 1: whole A'' per MMA pass; kz: 3D z-streaming slices
+    int terms = 1;             // 2: split B'' = B_hi + B_lo (SST_PREC_F16X2); K doubled
     int x_shift = 0;           // patch column of the window origin (TMA boxes start
                                // 16-byte aligned, so the patch begins lp cells early)
     int n_tiles() const { return tiles_x * tiles_y; }
@@ -37,6 +38,7 @@ struct DeviceImage {
     // byte offset inside one 8-tile B'' group (MN-major: row k at k * 16 B)
     std::vector<std::int32_t> gather_src, gather_dst;
     int worst_bank_conflict = 0;          // max lanes per bank over gather LDS sweeps
+    int lo_sweep0 = 0;                    // first gather sweep producing B_lo rows (= sweeps if terms 1)
 };
 
 /// Inputs are the reference compile products: compressed A'' (values as
@@ -48,5 +50,7 @@ DeviceImage build_device_image(const BatchGeometry& geo_in, std::size_t rows, st
 
 /// fp32 -> fp16 bits, round to nearest even (host side, for the A operand)
 std::uint16_t f32_to_f16_bits(float f);
+/// fp16 bits -> value (exact)
+double f16_bits_to_double(std::uint16_t h);
 
 }  // namespace stensor

@@ -24,6 +24,9 @@ PRESETS = ["Heat-1D", "1D5P", "Heat-2D", "Box-2D9P", "Star-2D13P", "Box-2D49P", 
            "Box-3D27P"]
 
 
+PRECISIONS = {"f16": _capi.SST_PREC_F16, "f16x2": _capi.SST_PREC_F16X2}
+
+
 def preset_names() -> list[str]:
     return list(PRESETS)
 
@@ -91,7 +94,11 @@ class SparseStencil:
     """A compiled stencil resident on one B200 (the device-side KernelPlan)."""
 
     def __init__(self, stencil: str | Compiled, grid_dims: Optional[Sequence[int]] = None,
-                 device: int = 0, r1: int = 16, r2: int = 8, fuse: int = 1):
+                 device: int = 0, r1: int = 16, r2: int = 8, fuse: int = 1, precision: str = "f16"):
+        """precision: "f16" (B'' rounded to binary16, the reference's round16 operand
+        semantics) or "f16x2" (B'' split into hi + lo binary16 terms: ~fp32 steps)."""
+        if precision not in PRECISIONS:
+            raise _capi.InvalidArgument(f"precision must be one of {sorted(PRECISIONS)}")
         self.compiled = stencil if isinstance(stencil, Compiled) else Compiled(
             stencil, grid_dims, r1, r2, fuse)
         self.grid_dims = self.compiled.grid_dims
@@ -99,6 +106,8 @@ class SparseStencil:
         self.k = int(self.compiled.info["k"])       # of the (possibly fused) operator
         self.r = (self.k - 1) // 2 // self.fuse     # radius of one original time step
         desc = self.compiled.plan_desc()
+        desc.precision = PRECISIONS[precision]
+        self.precision = precision
         h = C.c_void_p()
         check(lib().sst_plan_create(C.byref(desc), int(device), C.byref(h)))
         self._h = h
@@ -200,7 +209,7 @@ def valid_core(full: np.ndarray, steps: int, r: int) -> np.ndarray:
 
 
 def sparse_apply(stencil: str, grid: np.ndarray, steps: int, device: int = 0,
-                 fuse: int = 1) -> np.ndarray:
+                 fuse: int = 1, precision: str = "f16") -> np.ndarray:
     """Drop-in for stensor::direct_apply (stencil.hpp:72): valid-region result
     (extent N - steps*(k-1) per axis) computed on the B200. `fuse` > 1 applies
     the reference's temporal fusion (fuse_time_steps, stencil.cpp:272-347): one
@@ -209,7 +218,7 @@ def sparse_apply(stencil: str, grid: np.ndarray, steps: int, device: int = 0,
         raise _capi.InvalidArgument("steps must be >= 1")
     g = np.asarray(grid)
     f = fuse if fuse > 1 and steps % fuse == 0 else 1
-    eng = SparseStencil(stencil, list(g.shape), device=device, fuse=f)
+    eng = SparseStencil(stencil, list(g.shape), device=device, fuse=f, precision=precision)
     try:
         k1 = 2 * eng.r + 1
         for n in g.shape:

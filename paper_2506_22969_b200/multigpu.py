@@ -149,7 +149,7 @@ class SlabStencil:
     """A rank's share of a slab-decomposed stencil sweep on its B200."""
 
     def __init__(self, stencil: str, dims_per_rank: Sequence[int], rank: int = 0, world: int = 1,
-                 device: int = 0, group=None, fuse: int = 1):
+                 device: int = 0, group=None, fuse: int = 1, precision: str = "f16"):
         import torch
 
         from .engine import Compiled, SparseStencil
@@ -164,7 +164,7 @@ class SlabStencil:
         self.owned_dims = list(dims_per_rank)
         self.device = device
         self.group = group
-        self.eng = SparseStencil(stencil, self.local_dims, device=device, fuse=self.fuse)
+        self.eng = SparseStencil(stencil, self.local_dims, device=device, fuse=self.fuse, precision=precision)
         self.bufs = self.eng.bind_torch()
         self.flat = [b.view(torch.float32) for b in self.bufs]
         st = self.eng.storage

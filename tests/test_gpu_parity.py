@@ -268,3 +268,42 @@ def test_multistep_launch_equals_single_steps(gpu, monkeypatch, name, dims, step
     single, n_single = go(False)
     assert n_multi == 1 and n_single == steps
     assert np.array_equal(multi, single)
+
+
+# ---- split-operand precision (SST_PREC_F16X2): B'' = B_hi + B_lo, ~fp32 steps
+@pytest.mark.parametrize("name,dims", [("Box-2D9P", (300, 517)), ("Star-2D13P", (130, 129)),
+                                       ("Box-3D27P", (33, 17, 129)), ("Heat-3D", (20, 24, 40))])
+def test_f16x2_one_step_bit_exact(gpu, name, dims):
+    g = oracle.random_grid(dims, seed=4)
+    eng = SparseStencil(name, list(dims), precision="f16x2")
+    try:
+        got = valid_core(eng.apply_host(g.astype(np.float32), 1), 1, eng.r).astype(np.float64)
+    finally:
+        eng.close()
+    assert np.array_equal(got, oracle.direct_apply(name, g, 1))
+
+
+@pytest.mark.parametrize("name,dims,steps", [("Heat-2D", (512, 512), 100), ("Box-2D9P", (333, 290), 25),
+                                             ("Box-3D27P", (36, 40, 70), 10)])
+def test_f16x2_multi_step_accuracy(gpu, name, dims, steps):
+    """Tolerance: f32 accumulation of <= 49 exact products per step, values < 1:
+    max |err| <= 2^-20 (1 + T), and at least 100x below the f16 mode's error."""
+    g = oracle.random_grid(dims, seed=6)
+    want = oracle.direct_apply(name, g, steps)
+    errs = {}
+    for prec in ("f16", "f16x2"):
+        eng = SparseStencil(name, list(dims), precision=prec)
+        try:
+            got = valid_core(eng.apply_host(g.astype(np.float32), steps), steps, eng.r).astype(np.float64)
+        finally:
+            eng.close()
+        errs[prec] = np.abs(got - want).max()
+    assert errs["f16x2"] <= 2.0 ** -20 * (1 + steps), errs
+    assert errs["f16x2"] * 100 < errs["f16"], errs
+
+
+def test_f16x2_rejects_weights_not_exact_in_binary16(gpu):
+    doc = "name = tenth\ndims = 2\nshape = star\nk = 3\npoint = 0 0 : 0.1\npoint = 0 1 : 0.9\n"
+    with pytest.raises(ValueError):
+        SparseStencil(doc, [64, 64], precision="f16x2")
+    SparseStencil(doc, [64, 64], precision="f16").close()  # f16 rounds A'' and is accepted
