@@ -157,12 +157,14 @@ Variant make_stream_variant() {
 // experiments; SST_A_SMEM=1 skips the A''-in-TMEM variants)
 const Variant* variants(int& n) {
     static const Variant v[] = {
-        // 2D (measured order, tools/ablate.py): 0 smem-A 8x3 (Box-2D9P 8192^2: 89.6 us),
-        // 1 TMEM-A 4x4 (Star-2D13P 16384^2: 435 us vs 462 for smem-A 4x4), then the rest
-        make_variant<2, 8, 3, false>(), make_variant<2, 4, 4, true>(), make_variant<2, 8, 3, true>(),
+        // 2D (measured order, tools/ablate.py): 0 TMEM-A 8x3 (Box-2D9P 8192^2 multi-step
+        // 85.7 us = smem-A; Heat-2D 4096^2 single L2-cold launch 28.9 vs 30.7 us), 1 TMEM-A
+        // 4x4 (Star-2D13P 16384^2: 417 us vs 433 for smem-A 4x4), 2 smem-A 8x3, then the rest
+        make_variant<2, 8, 3, true>(), make_variant<2, 4, 4, true>(), make_variant<2, 8, 3, false>(),
         make_variant<2, 4, 4, false>(), make_variant<2, 4, 2, true>(), make_variant<2, 8, 2, false>(),
         make_variant<2, 4, 2, false>(), make_variant<2, 8, 4, false>(), make_variant<2, 8, 4, true>(),
-        // 3D z-streaming (9-15): TMEM-A TYB 4 NP 4 (Box-3D27P 512^3: 206 us vs 222 smem-A), ...
+        make_variant<2, 8, 2, true>(),
+        // 3D z-streaming (10-16): TMEM-A TYB 4 NP 4 (Box-3D27P 512^3: 206 us vs 222 smem-A), ...
         make_stream_variant<4, 4, 3, true>(), make_stream_variant<4, 3, 3, true>(),
         make_stream_variant<8, 3, 3, true>(), make_stream_variant<4, 2, 3, true>(),
         make_stream_variant<4, 6, 3, true>(), make_stream_variant<4, 4, 3, false>(),
