@@ -122,11 +122,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch_desc(&maps.ring[p.src]);
     }
     if (warp == 1) tmem_alloc(tmem_slot, static_cast<uint32_t>(p.tmem_cols));
-    stage_constants<AT>(p, sA, sB, sGsrc, sGdst);
-    fence_proxy_async_smem();
+    uint64_t* pbar = reinterpret_cast<uint64_t*>(smem + L.pbar);
+    if (threadIdx.x == 0) {
+        mbar_init(pbar, 1);
+        fence_mbar_init();
+        stage_constants_issue<AT>(p, sA, sB, sGsrc, sGdst, pbar);
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    mbar_wait(pbar, 0);  // constants in smem
+    const unsigned long long t_mid = p.trace ? global_ns() : 0ull;  // constants staged, TMEM allocated
     const uint32_t tmem = *tmem_slot;
     const TmemCols tc = tmem_budget(NACC * N, static_cast<uint32_t>(p.nks), AT);
     const uint32_t e_col = tc.e_col;  // metadata after the accumulator ring, then A'' (AT)
@@ -317,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         unsigned long long* t = p.trace + 4 * blockIdx.x;
         t[0] = smid();
         t[1] = t_start;
-        t[2] = t_main;
+        t[2] = (p.debug_mode & 1024) ? t_mid : t_main;  // profiling: prologue split
         t[3] = global_ns();
     }
     if (warp == 1) {

@@ -91,25 +91,24 @@ __host__ __device__ inline void tile_of_column(int n, int& tx, int& ty) {
     tx = 2 * c + (m & 1);
 }
 
-// Prologue staging, global -> smem with all threads, coalesced 16-byte loads and
-// no intervening asm barriers (one memory round trip): the A'' image (to its smem
-// home, or to `scratch` when it goes to TMEM), the TMEM metadata words (to
-// `scratch`) and the gather tables. `scratch` is the B'' / staging / patch region,
-// idle until the main loop; the host checks it is large enough.
+// Prologue staging, global -> smem by 1D bulk copies (TMA engine, one thread;
+// a thread-strided copy loop is load-latency bound: 4.3 us for the 81 KiB of the
+// 3D constants): the A'' image (to its smem home, or to `scratch` when it goes to
+// TMEM), the TMEM metadata words (to `scratch`) and the gather tables. `scratch`
+// is the B'' / staging / patch region, idle until the main loop; the host checks it
+// is large enough. Call from one thread after pbar's init; everyone then waits on
+// pbar (phase 0) after a CTA barrier.
 template <bool AT>
-__device__ __forceinline__ void stage_constants(const StepParams& p, uint8_t* sA, uint8_t* scratch,
-                                                int32_t* sGsrc, int32_t* sGdst) {
-    const int nA = p.nks * 4096 / 16;
-    uint4* dA = reinterpret_cast<uint4*>(AT ? scratch : sA);
-    for (int i = threadIdx.x; i < nA; i += kThreads) dA[i] = p.a_img[i];
-    const int nE = p.nks * 128 / 4;
-    uint4* dE = reinterpret_cast<uint4*>(scratch + (AT ? p.nks * 4096 : 0));
-    const uint4* gE = reinterpret_cast<const uint4*>(p.e_words);
-    for (int i = threadIdx.x; i < nE; i += kThreads) dE[i] = gE[i];
-    for (int i = threadIdx.x; i < p.k_pad; i += kThreads) {  // k_pad/32 sweeps x 32 lanes
-        sGsrc[i] = p.gsrc[i];
-        sGdst[i] = p.gdst[i];
-    }
+__device__ __forceinline__ void stage_constants_issue(const StepParams& p, uint8_t* sA, uint8_t* scratch,
+                                                      int32_t* sGsrc, int32_t* sGdst, uint64_t* pbar) {
+    const uint32_t a_bytes = static_cast<uint32_t>(p.nks) * 4096u;
+    const uint32_t e_bytes = static_cast<uint32_t>(p.nks) * 512u;
+    const uint32_t t_bytes = static_cast<uint32_t>(p.k_pad) * 4u;
+    ptx::mbar_arrive_expect_tx(pbar, a_bytes + e_bytes + 2 * t_bytes);
+    ptx::bulk_copy_g2s(AT ? scratch : sA, p.a_img, a_bytes, pbar);
+    ptx::bulk_copy_g2s(scratch + (AT ? a_bytes : 0u), p.e_words, e_bytes, pbar);
+    ptx::bulk_copy_g2s(sGsrc, p.gsrc, t_bytes, pbar);
+    ptx::bulk_copy_g2s(sGdst, p.gdst, t_bytes, pbar);
 }
 __host__ __device__ inline uint32_t prologue_scratch_bytes(int nks, bool a_in_tmem) {
     return static_cast<uint32_t>(nks) * ((a_in_tmem ? 4096u : 0u) + 512u);

@@ -24,6 +24,7 @@ namespace sst {
 
 struct SmemLayout {
     uint32_t a, b, b_stride, p, p_stride, s, s_stride, gsrc, gdst, bars, tmem_slot, total;
+    uint32_t pbar;  // prologue mbarrier (constant staging by bulk copy)
     uint32_t ring;  // 3D stream kernel: right-edge ring-value cache (kRingSlots x TYB*8 x 4 floats)
 };
 
@@ -55,6 +56,8 @@ __host__ __device__ inline SmemLayout smem_layout_generic(int nks, int k_pad, in
     o += static_cast<uint32_t>(k_pad) * 4u;
     L.bars = o = align_up(o, 8);
     o += nbars * 8;
+    L.pbar = o;
+    o += 8;
     L.tmem_slot = o;
     o += 16;
     L.total = align_up(o, 128);
@@ -156,11 +159,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
     if (warp == 1) tmem_alloc(tmem_slot, static_cast<uint32_t>(p.tmem_cols));
-    stage_constants<AT>(p, sA, sB, sGsrc, sGdst);
-    fence_proxy_async_smem();
+    uint64_t* pbar = reinterpret_cast<uint64_t*>(smem + L.pbar);
+    if (threadIdx.x == 0) {
+        mbar_init(pbar, 1);
+        fence_mbar_init();
+        stage_constants_issue<AT>(p, sA, sB, sGsrc, sGdst, pbar);
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    mbar_wait(pbar, 0);  // constants in smem
     const uint32_t tmem = *tmem_slot;
     // TMEM: two accumulators, the metadata columns, then (AT) the A'' operand
     const TmemCols tc = tmem_budget(2 * N, static_cast<uint32_t>(p.nks), AT);
