@@ -204,6 +204,8 @@ struct sst_plan {
     bool owns_buf = false;
     sst::MapSet maps{};       // in[i]: patch loads over buffer i (whole storage);
                               // out[i]: stores into buffer i, clipped to the interior (and row window)
+    uint32_t* d_sched = nullptr;  // dynamic batch counter of single-step 2D launches
+    uint32_t sched_base = 0;
     uint32_t* d_flags = nullptr;  // per-batch step counters of multi-step launches
     int flags_n = 0;
     uint32_t flag_base = 0;
@@ -222,6 +224,7 @@ struct sst_plan {
         cudaFree(d_gsrc);
         cudaFree(d_gdst);
         cudaFree(d_flags);
+        cudaFree(d_sched);
         if (owns_buf) {
             cudaFree(buf[0]);
             cudaFree(buf[1]);
@@ -358,15 +361,20 @@ struct sst_plan {
     }
 
     // Launch `nsteps` operator applications starting from buffer src; returns the
-    // buffer holding the result. Multi-step launches need the full window and a
-    // multi-step variant (SST_MULTISTEP=0 forces one launch per step).
+    // buffer holding the result. Multi-step launches (opt-in, SST_MULTISTEP=1) need
+    // the full window and a multi-step variant.
     int launch(int src, uint64_t nsteps, cudaStream_t st) {
         sst::StepParams p = step_params(src);
         if (p.nbatch <= 0 || nsteps == 0) return src;
         const int grid = grid_size(p);
         if (p.slow_lo != map_lo || p.slow_hi != map_hi) make_tmaps();  // window changed
-        const char* ms_e = std::getenv("SST_MULTISTEP");  // read per call (tests toggle it)
-        const bool ms_env = !(ms_e && std::atoi(ms_e) == 0);
+        // Default: one launch per step, batches drawn dynamically, PDL overlapping
+        // consecutive steps (Box-2D9P 8192^2: 83.4 us/step vs 86.4 for the
+        // multi-step dataflow launch, whose static batch ownership inherits the
+        // 15-20 % spread of per-SM speed). SST_MULTISTEP=1 selects the multi-step
+        // launch (read per call: tests toggle it).
+        const char* ms_e = std::getenv("SST_MULTISTEP");
+        const bool ms_env = ms_e && std::atoi(ms_e) != 0;
         const bool full = !(y_hi > y_lo);
         const bool multi = ms_env && variant->multistep && full && nsteps > 1;
         if (multi && flags_n < p.nbatch) {
@@ -386,7 +394,19 @@ struct sst_plan {
             p.nsteps = static_cast<int32_t>(chunk);
             p.flags = d_flags;
             p.flag_base = flag_base;
+            // single-step 2D launches draw batches from a counter (load balance: the
+            // static stride leaves a 15-20 % spread of CTA finish times); SST_DYN=0 off
+            const char* dyn_e = std::getenv("SST_DYN");
+            const bool dyn = !multi && variant->multistep && !(dyn_e && std::atoi(dyn_e) == 0);
+            if (dyn && !d_sched) {
+                ck(cudaMalloc(&d_sched, 4), "cudaMalloc(sched)");
+                ck(cudaMemsetAsync(d_sched, 0, 4, st), "cudaMemsetAsync(sched)");
+                sched_base = 0;
+            }
+            p.sched = dyn ? d_sched : nullptr;
+            p.sched_base = sched_base;
             variant->launch(grid, smem, st, maps, p, multi);
+            if (dyn) sched_base += static_cast<uint32_t>(p.nbatch + grid);
             ck(cudaGetLastError(), "kernel launch");
             ++launches;
             if (multi) {  // per-CTA progress counters advance by nper iterations per step

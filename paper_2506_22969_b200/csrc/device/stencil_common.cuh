@@ -54,6 +54,8 @@ struct StepParams {
     int32_t tmem_cols;         // TMEM allocation (power of two >= the kernel's column budget)
     int32_t zchunk;            // 3D stream kernel: output planes per (band, z-chunk) run; 0 = whole column
     int32_t lo_sweep0;         // first gather sweep writing B_lo rows (SST_PREC_F16X2); = k_pad/32 otherwise
+    uint32_t* sched;           // 2D single-step launches: global batch counter (dynamic scheduling), or null
+    uint32_t sched_base;       // counter value at launch start
     unsigned long long* trace; // profiling only (sst_plan_set_trace): per CTA {smid, t_start, t_main, t_end}
 };
 

@@ -64,10 +64,22 @@ __host__ __device__ inline SmemLayout smem_layout_generic(int nks, int k_pad, in
     return L;
 }
 
+// Dynamic batch scheduling of single-step launches: the producer draws batch
+// indices from a global counter and hands them to the other roles through a ring
+// of kBidSlots (index, mbarrier) slots (reuse is safe: the producer cannot run
+// kBidSlots iterations ahead of the epilogue through the patch / B'' / accumulator
+// rings, 3 + 2 + 2 deep).
+constexpr int kBidSlots = 16;
+
 template <int TYB, int NP, bool AT>
 __host__ __device__ inline SmemLayout smem_layout(int nks, int k_pad, int patch_w, int patch_h,
                                                   int planes) {
-    return smem_layout_generic<TYB>(nks, k_pad, patch_w, patch_h, planes, NP, 2, 2 * NP + 8, kStageBufs, AT);
+    static_assert(kBidSlots > NP + 4, "batch-index ring vs pipeline depth");
+    SmemLayout L = smem_layout_generic<TYB>(nks, k_pad, patch_w, patch_h, planes, NP, 2, 2 * NP + 8 + kBidSlots,
+                                            kStageBufs, AT);
+    L.ring = align_up(L.total, 16);  // the batch-index ring (int32 x kBidSlots)
+    L.total = align_up(L.ring + kBidSlots * 4, 128);
+    return L;
 }
 
 // Multi-step dataflow. Every CTA walks the same number of iterations per step
@@ -135,6 +147,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* b_empty = b_full + 2;
     uint64_t* d_full = b_full + 4;
     uint64_t* d_empty = b_full + 6;
+    uint64_t* bid_full = b_full + 8;  // [kBidSlots]
+    int32_t* sBid = reinterpret_cast<int32_t*>(smem + L.ring);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem_slot);
 
     const int warp = threadIdx.x / 32;
@@ -152,6 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&d_full[s], 1);
             mbar_init(&d_empty[s], kEpiWarps);
         }
+        for (int s = 0; s < kBidSlots; ++s) mbar_init(&bid_full[s], 1);
         fence_mbar_init();
         for (int i = 0; i < 2; ++i) {
             tma_prefetch_desc(&maps.in[i]);
@@ -203,6 +218,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         Z0 = b / (nbx * nby) + (DIMS == 3 ? p.slow_lo : 0);
     };
     const bool multi = p.nsteps > 1;
+    // single-step launches with a scheduler counter draw batches dynamically
+    const bool dyn = p.sched != nullptr && !multi;
+    auto next_bid = [&](int r) {  // consumers: batch index of real iteration r (-1: done)
+        mbar_wait(&bid_full[r % kBidSlots], (r / kBidSlots) & 1);
+        return sBid[r % kBidSlots];
+    };
 
     if ((p.debug_mode & 32) && warp < kEpiWarp0) {
         // store-only ablation: only the epilogue runs (writes zeros)
@@ -212,7 +233,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t pbytes = static_cast<uint32_t>(p.patch_w * p.patch_h * p.patch_planes) * 4u;
         uint32_t polls = 0, known = p.flag_base;  // min over all progress counters seen
         int r = 0;                                // real (non no-op) iterations
-        for (int j = 0; j < total; ++j) {
+        if (dyn) {
+            // the next index is drawn one batch ahead so the atomic's latency hides
+            // behind the current batch's wait / issue
+            uint32_t nxt = lane == 0 ? atomicAdd(p.sched, 1u) - p.sched_base : 0u;
+            for (;; ++r) {
+                int b = -1;
+                if (lane == 0) {
+                    b = nxt < static_cast<uint32_t>(p.nbatch) ? static_cast<int>(nxt) : -1;
+                    if (b >= 0) nxt = atomicAdd(p.sched, 1u) - p.sched_base;
+                    sBid[r % kBidSlots] = b;
+                    mbar_arrive(&bid_full[r % kBidSlots]);
+                }
+                b = __shfl_sync(0xffffffffu, b, 0);
+                if (b < 0) break;
+                int X0, Y0, Z0;
+                batch_coords(b, X0, Y0, Z0);
+                if (lane == 0) {
+                    const int s = r % NP;
+                    mbar_wait(&patch_empty[s], ((r / NP) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&patch_full[s], pbytes);
+                    void* dst = sP + s * L.p_stride;
+                    if (DIMS == 2)
+                        tma_load_2d(dst, &maps.in[p.src & 1], &patch_full[s], X0 + p.load_x0, Y0);
+                    else
+                        tma_load_3d(dst, &maps.in[p.src & 1], &patch_full[s], X0 + p.load_x0, Y0, Z0);
+                }
+                __syncwarp();
+            }
+        }
+        for (int j = 0; j < (dyn ? 0 : total); ++j) {
             int t, b, X0, Y0, Z0;
             batch_of(j, t, b);
             if (b >= p.nbatch) continue;
@@ -251,12 +301,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t b_sbo = static_cast<uint32_t>(p.k_pad) * 16u;
         const uint32_t a0 = smem_u32(sA);
         int r = 0;
-        for (int j = 0; j < total; ++j, ++r) {
+        for (int j = 0; dyn || j < total; ++j, ++r) {
             int t, b;
-            batch_of(j, t, b);
-            if (b >= p.nbatch) {
-                --r;
-                continue;
+            if (dyn) {
+                if (next_bid(r) < 0) break;
+            } else {
+                batch_of(j, t, b);
+                if (b >= p.nbatch) {
+                    --r;
+                    continue;
+                }
             }
             const int s = r & 1;
             const uint32_t ph = (r >> 1) & 1;
@@ -292,12 +346,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t gstride = static_cast<uint32_t>(p.k_pad) * 16u;  // bytes per 8-tile group
         const int nsweeps = (active && !(p.debug_mode & 2)) ? p.k_pad / 32 : 0;
         int r = 0;
-        for (int j = 0; j < total; ++j, ++r) {
+        for (int j = 0; dyn || j < total; ++j, ++r) {
             int t, b;
-            batch_of(j, t, b);
-            if (b >= p.nbatch) {
-                --r;
-                continue;
+            if (dyn) {
+                if (next_bid(r) < 0) break;
+            } else {
+                batch_of(j, t, b);
+                if (b >= p.nbatch) {
+                    --r;
+                    continue;
+                }
             }
             const int ps = r % NP;
             const uint32_t pph = (r / NP) & 1;
@@ -333,12 +391,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             st_relaxed_gpu(p.flags + blockIdx.x, p.flag_base + static_cast<uint32_t>(upto));
             published = upto;
         };
-        for (int j = 0; j < total; ++j) {
-            int t, b, X0, Y0, Z0;
-            batch_of(j, t, b);
-            if (b >= p.nbatch) {  // no-op iteration: nothing to store
-                committed = j + 1;
-                continue;
+        for (int j = 0; dyn || j < total; ++j) {
+            int t = 0, b, X0, Y0, Z0;
+            if (dyn) {
+                b = next_bid(r);
+                if (b < 0) break;
+            } else {
+                batch_of(j, t, b);
+                if (b >= p.nbatch) {  // no-op iteration: nothing to store
+                    committed = j + 1;
+                    continue;
+                }
             }
             batch_coords(b, X0, Y0, Z0);
             const int s = r & 1;

@@ -153,9 +153,9 @@ def test_torch_device_buffers_and_launch_count(gpu):
     eng.upload(src, 0)
     before = eng.stats()["launches"]
     dst = eng.run(7, src=0)
-    # 2D: one multi-step launch runs all 7 time steps (per-batch dataflow, no
-    # grid-wide barrier); the result lands in the other buffer after an odd count
-    assert eng.stats()["launches"] - before == 1 and dst == 1
+    # one launch per time step (dynamic batch scheduling, PDL between steps); the
+    # result lands in the other buffer after an odd count
+    assert eng.stats()["launches"] - before == 7 and dst == 1
     out = torch.empty(dims, dtype=torch.float32, device="cuda")
     eng.download(dst, out)
     torch.cuda.synchronize()
@@ -241,8 +241,8 @@ def test_every_variant_bit_exact(gpu, monkeypatch, variant):
         assert np.all(np.abs(got - want) <= ulp), (name, variant, np.abs(got - want).max())
 
 
-# The multi-step dataflow launch (one launch, T steps, cross-CTA progress counters)
-# must equal T single-step launches bitwise: same arithmetic per step, so any
+# The multi-step dataflow launch (SST_MULTISTEP=1: one launch, T steps, cross-CTA
+# progress counters) must equal T single-step launches bitwise: same arithmetic per step, so any
 # ordering bug (a batch loading a neighbour's halo before it was stored) shows up
 # as a mismatch. Shapes cover grids with fewer batches than SMs, a single batch
 # row or column, ragged edges, and many steps.
@@ -254,8 +254,9 @@ def test_every_variant_bit_exact(gpu, monkeypatch, variant):
 def test_multistep_launch_equals_single_steps(gpu, monkeypatch, name, dims, steps):
     g = oracle.random_grid(dims, seed=21).astype(np.float32)
 
-    def go(multistep):
+    def go(multistep, dynamic=True):
         monkeypatch.setenv("SST_MULTISTEP", "1" if multistep else "0")
+        monkeypatch.setenv("SST_DYN", "1" if dynamic else "0")
         eng = SparseStencil(name, list(dims))
         try:
             before = eng.stats()["launches"]
@@ -265,9 +266,11 @@ def test_multistep_launch_equals_single_steps(gpu, monkeypatch, name, dims, step
             eng.close()
 
     multi, n_multi = go(True)
-    single, n_single = go(False)
+    single, n_single = go(False)              # default: dynamic batch scheduling
+    static, _ = go(False, dynamic=False)      # static batch striding
     assert n_multi == 1 and n_single == steps
     assert np.array_equal(multi, single)
+    assert np.array_equal(static, single)
 
 
 # ---- split-operand precision (SST_PREC_F16X2): B'' = B_hi + B_lo, ~fp32 steps
