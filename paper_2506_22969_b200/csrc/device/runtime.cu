@@ -397,7 +397,10 @@ struct sst_plan {
             // single-step 2D launches draw batches from a counter (load balance: the
             // static stride leaves a 15-20 % spread of CTA finish times); SST_DYN=0 off
             const char* dyn_e = std::getenv("SST_DYN");
-            const bool dyn = !multi && variant->multistep && !(dyn_e && std::atoi(dyn_e) == 0);
+            // (few batches per CTA: static striding measured faster, e.g. Heat-2D 4096^2
+            // L2-cold 28.6 vs 29.9 us; SST_DYN=1 forces dynamic, 0 static)
+            const bool dyn = !multi && variant->multistep &&
+                             (dyn_e ? std::atoi(dyn_e) != 0 : p.nbatch >= 24 * grid);
             if (dyn && !d_sched) {
                 ck(cudaMalloc(&d_sched, 4), "cudaMalloc(sched)");
                 ck(cudaMemsetAsync(d_sched, 0, 4, st), "cudaMemsetAsync(sched)");
@@ -406,7 +409,7 @@ struct sst_plan {
             p.sched = dyn ? d_sched : nullptr;
             p.sched_base = sched_base;
             variant->launch(grid, smem, st, maps, p, multi);
-            if (dyn) sched_base += static_cast<uint32_t>(p.nbatch + grid);
+            if (dyn) sched_base += static_cast<uint32_t>(p.nbatch);  // nbatch - grid draws + grid final ones
             ck(cudaGetLastError(), "kernel launch");
             ++launches;
             if (multi) {  // per-CTA progress counters advance by nper iterations per step

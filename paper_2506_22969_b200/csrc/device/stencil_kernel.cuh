@@ -234,14 +234,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t polls = 0, known = p.flag_base;  // min over all progress counters seen
         int r = 0;                                // real (non no-op) iterations
         if (dyn) {
-            // the next index is drawn one batch ahead so the atomic's latency hides
+            // a CTA's first batch is blockIdx.x, later ones G + counter draws; the
+            // next index is drawn one batch ahead so the atomic's latency hides
             // behind the current batch's wait / issue
-            uint32_t nxt = lane == 0 ? atomicAdd(p.sched, 1u) - p.sched_base : 0u;
+            uint32_t nxt = blockIdx.x;
             for (;; ++r) {
                 int b = -1;
                 if (lane == 0) {
                     b = nxt < static_cast<uint32_t>(p.nbatch) ? static_cast<int>(nxt) : -1;
-                    if (b >= 0) nxt = atomicAdd(p.sched, 1u) - p.sched_base;
+                    if (b >= 0) nxt = static_cast<uint32_t>(G) + atomicAdd(p.sched, 1u) - p.sched_base;
                     sBid[r % kBidSlots] = b;
                     mbar_arrive(&bid_full[r % kBidSlots]);
                 }
