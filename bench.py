@@ -66,30 +66,60 @@ def _dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region: NVML every
+    10 ms (nvidia-smi every 200 ms if NVML is unavailable)."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap"}
 
     def __init__(self, gpu: int):
         self.gpu = gpu
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, [reasons])
         self._stop = threading.Event()
         self._t = None
 
-    def start(self):
+    def _nvml(self):
+        import pynvml
+
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+
+        def sample():
+            mask = get_reasons(h)
+            return (float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)), float(mx),
+                    [n for bit, n in self.REASONS.items() if mask & bit])
+        return sample
+
+    def _smi(self):
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+        def sample():
+            out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                 timeout=5).stdout.strip()
+            r = [x.strip() for x in out.split(",")]
+            return (float(r[0]), float(r[1]), [names[i] for i in range(4) if r[2 + i].lower() == "active"])
+        return sample
+
+    def start(self):
+        try:
+            sample, period = self._nvml(), 0.01
+        except Exception:
+            sample, period = self._smi(), 0.2
 
         def run():
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True,
-                                         text=True, timeout=5).stdout.strip()
-                    if out:
-                        self.rows.append([x.strip() for x in out.split(",")])
+                    self.rows.append(sample())
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                self._stop.wait(period)
 
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
@@ -100,13 +130,9 @@ class ClockSampler:
             self._t.join(timeout=10)
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 2 + i and r[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows),
+                "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": sorted({n for r in self.rows for n in r[2]}),
                 "samples": len(self.rows)}
 
 
