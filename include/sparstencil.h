@@ -67,7 +67,12 @@ typedef struct sst_compiled sst_compiled;
 
 /* Compile a stencil for a grid. `stencil` is a preset name (Heat-2D, ...) or a
  * spec document (docs/formats.md:3-30). r1/r2 = 0 selects the tcgen05 layout
- * explorer (r1*r2 = 128); fuse >= 1 applies fuse_time_steps first. */
+ * explorer (r1*r2 = 128); fuse >= 1 applies fuse_time_steps first.
+ * A 1D stencil with (r1, r2) = (16, 8) (the device layout) is FOLDED: the 1D
+ * grid of N cells is viewed as R rows of W interior cells (rows overlapping by
+ * the halo, W a multiple of 128) and the stencil embedded as a 2D star stencil
+ * acting along the rows; the device runs that 2D operator (fold_n / fold_w in
+ * sst_compile_info). Other (r1, r2) compile the reference's 1D layout (r2 = 1). */
 SST_API sst_status sst_compile(const char* stencil, const uint64_t* grid_dims, int ndims, int r1, int r2,
                        uint64_t fuse, sst_compiled** out);
 SST_API void sst_compiled_destroy(sst_compiled* c);
@@ -83,7 +88,9 @@ typedef struct sst_compile_info {
     uint64_t window_w;      /* wv = kx + r1 - 1 */
     uint64_t window_h;      /* wu = ky + r2 - 1 */
     uint64_t window_d;      /* kz (3D) or 1 */
-    uint64_t grid_dims[3];
+    uint64_t grid_dims[3];  /* the compiled grid (a 1D fold: the 2D view) */
+    uint64_t fold_n;        /* 1D stencils on the device layout: length N of the 1D grid, else 0 */
+    uint64_t fold_w;        /* ... and the fold width W (view rows of W interior cells) */
 } sst_compile_info;
 
 SST_API sst_status sst_compiled_info(const sst_compiled* c, sst_compile_info* info);
@@ -113,6 +120,9 @@ typedef struct sst_plan_desc {
     uint64_t window_w, window_h, window_d;
     int32_t precision;        /* SST_PREC_F16 or SST_PREC_F16X2 */
     uint32_t fuse;            /* time steps per operator application (fuse_time_steps); 0 = 1 */
+    uint64_t fold_n;          /* > 0: 1D grid of fold_n cells folded into the 2D view grid_dims
+                               * (rows of fold_w interior cells, overlapping by the halo) */
+    uint64_t fold_w;
 } sst_plan_desc;
 
 /* Pointers into the compiled object; valid while `c` lives. */

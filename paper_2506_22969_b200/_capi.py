@@ -62,7 +62,7 @@ class CompileInfo(C.Structure):
                 ("cols", C.c_uint64), ("p", C.c_uint64), ("align_cols", C.c_uint64),
                 ("used_blossom", C.c_int32), ("refined", C.c_int32),
                 ("window_w", C.c_uint64), ("window_h", C.c_uint64), ("window_d", C.c_uint64),
-                ("grid_dims", C.c_uint64 * 3)]
+                ("grid_dims", C.c_uint64 * 3), ("fold_n", C.c_uint64), ("fold_w", C.c_uint64)]
 
 
 class PlanDesc(C.Structure):
@@ -71,7 +71,8 @@ class PlanDesc(C.Structure):
                 ("a_values", C.POINTER(C.c_double)), ("a_meta", C.POINTER(C.c_uint8)),
                 ("col_origin", C.POINTER(C.c_uint64)),
                 ("window_w", C.c_uint64), ("window_h", C.c_uint64), ("window_d", C.c_uint64),
-                ("precision", C.c_int32), ("fuse", C.c_uint32)]
+                ("precision", C.c_int32), ("fuse", C.c_uint32), ("fold_n", C.c_uint64),
+                ("fold_w", C.c_uint64)]
 
 
 class Storage(C.Structure):

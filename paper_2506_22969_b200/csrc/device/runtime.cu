@@ -216,6 +216,8 @@ struct sst_plan {
     int debug_mode = 0;  // SST_DEBUG_MODE (ablation experiments only)
     uint64_t fuse = 1;   // original time steps per launch
     int load_x0 = 0;     // storage column of a batch's patch start, relative to X0
+    uint64_t fold_n = 0, fold_w = 0;  // 1D grid folded into the 2D view (see sst_compile)
+    float* d_ring_save = nullptr;     // fold: the r right-ring cells, restored after a run
 
     ~sst_plan() {
         cudaSetDevice(device);
@@ -225,6 +227,7 @@ struct sst_plan {
         cudaFree(d_gdst);
         cudaFree(d_flags);
         cudaFree(d_sched);
+        cudaFree(d_ring_save);
         if (owns_buf) {
             cudaFree(buf[0]);
             cudaFree(buf[1]);
@@ -265,6 +268,30 @@ struct sst_plan {
         const cuuint64_t gstride[2] = {storage.row_pitch * 4, storage.plane_pitch * 4};
         int32_t lo, hi;
         window(lo, hi);
+        if (fold_n) {
+            // 1D fold: view row i = storage cells [i W, i W + lp + W + 2r) — rows overlap
+            // by the halo (a TMA map may have row stride < row extent) — so every cell's
+            // 1D neighbourhood lies in its view row; stores: rows of W interior cells
+            // starting at the first interior cell lp + r
+            if (y_hi > y_lo) throw std::invalid_argument("row windows are not supported for a 1D fold");
+            const cuuint64_t fstride[1] = {fold_w * 4};
+            const cuuint64_t rows = static_cast<cuuint64_t>(gy - 2 * r);
+            for (int i = 0; i < 2; ++i) {
+                const cuuint64_t gdim[2] = {(storage.left_pad + fold_w + 2 * r + 3) / 4 * 4, rows};
+                const cuuint32_t box[2] = {static_cast<cuuint32_t>(img.geo.patch_w),
+                                           static_cast<cuuint32_t>(img.geo.patch_h)};
+                encode(&maps.in[i], 2, buf[i], gdim, fstride, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+                const cuuint64_t odim[2] = {fold_w, rows};
+                const cuuint32_t obox[2] = {static_cast<cuuint32_t>(sst::kBoxW),
+                                            static_cast<cuuint32_t>(tiles_y * sst::kTileH)};
+                encode(&maps.out[i], 2, buf[i] + storage.left_pad + r, odim, fstride, obox,
+                       CU_TENSOR_MAP_SWIZZLE_128B);
+            }
+            map_lo = lo;
+            map_hi = hi;
+            tmap_ok = true;
+            return;
+        }
         for (int i = 0; i < 2; ++i) {
             // loads: the whole storage buffer; boxes start on 16-byte aligned columns
             const cuuint64_t gdim[3] = {storage.row_pitch, static_cast<cuuint64_t>(gy),
@@ -345,6 +372,7 @@ struct sst_plan {
         p.tmem_cols = tmem_cols;
         p.zchunk = zchunk;
         p.lo_sweep0 = img.lo_sweep0;
+        p.load_y0 = fold_n ? -r : 0;  // fold: view rows have no ring rows above them
         p.trace = trace;
         return p;
     }
@@ -376,7 +404,9 @@ struct sst_plan {
         const char* ms_e = std::getenv("SST_MULTISTEP");
         const bool ms_env = ms_e && std::atoi(ms_e) != 0;
         const bool full = !(y_hi > y_lo);
-        const bool multi = ms_env && variant->multistep && full && nsteps > 1;
+        // (a fold's view rows depend on the next row's first cells: outside the
+        // multi-step kernel's 3 x 3 batch neighbourhood, so folds run per step)
+        const bool multi = ms_env && variant->multistep && full && nsteps > 1 && !fold_n;
         if (multi && flags_n < p.nbatch) {
             cudaFree(d_flags);
             d_flags = nullptr;
@@ -387,6 +417,15 @@ struct sst_plan {
         }
         int cur = src;
         uint64_t left = nsteps;
+        // fold: the last view row also computes the r right-ring cells (and pad); the
+        // valid core never reads them after step 0 (its dependency cone stays inside
+        // the interior), so they are restored only once the run is over
+        const size_t ring_off = static_cast<size_t>(storage.left_pad + fold_n - r);
+        if (fold_n && r > 0) {
+            if (!d_ring_save) ck(cudaMalloc(&d_ring_save, static_cast<size_t>(r) * 4), "cudaMalloc(ring)");
+            ck(cudaMemcpyAsync(d_ring_save, buf[src] + ring_off, static_cast<size_t>(r) * 4,
+                               cudaMemcpyDeviceToDevice, st), "cudaMemcpyAsync(ring save)");
+        }
         while (left > 0) {
             // chunks keep flag counters far from wrap-around between resets
             const uint64_t chunk = multi ? std::min<uint64_t>(left, 1u << 16) : 1;
@@ -419,6 +458,9 @@ struct sst_plan {
             cur = (cur + static_cast<int>(chunk & 1)) & 1;
             left -= chunk;
         }
+        if (fold_n && r > 0)
+            ck(cudaMemcpyAsync(buf[cur] + ring_off, d_ring_save, static_cast<size_t>(r) * 4,
+                               cudaMemcpyDeviceToDevice, st), "cudaMemcpyAsync(ring restore)");
         return cur;
     }
 };
@@ -440,6 +482,8 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
         const int terms = d->precision == SST_PREC_F16X2 ? 2 : 1;
         if (d->dims != 2 && d->dims != 3)
             throw std::invalid_argument("device path supports 2D and 3D stencils (m' = 128 needs r2 > 1)");
+        if (d->fold_n && (d->dims != 2 || d->fold_w % 128 != 0 || d->fold_w == 0))
+            throw std::invalid_argument("bad 1D fold");
         if (d->r1 != sst::kTileW || d->r2 != sst::kTileH || d->rows != 128)
             throw std::invalid_argument("device path needs the (r1, r2) = (16, 8) layout");
         if (d->k < 1 || d->k % 2 == 0) throw std::invalid_argument("k must be odd and >= 1");
@@ -551,6 +595,8 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
         if (const char* dm = std::getenv("SST_DEBUG_MODE")) P->debug_mode = std::atoi(dm);
         if (const char* zc = std::getenv("SST_ZCHUNK")) P->zchunk = std::atoi(zc);
 
+        P->fold_n = d->fold_n;
+        P->fold_w = d->fold_w;
         P->storage.left_pad = lp;
         P->storage.row_pitch = (lp + static_cast<uint64_t>(P->gx) + aln - 1) / aln * aln;
         {  // room for the 3D stream kernel's full last 16-byte store chunk
@@ -560,6 +606,14 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
         }
         P->storage.plane_pitch = P->storage.row_pitch * static_cast<uint64_t>(P->gy);
         P->storage.bytes = P->storage.plane_pitch * static_cast<uint64_t>(P->gz) * 4;
+        if (P->fold_n) {  // 1D: contiguous cells, element p at left_pad + p; room for the
+                          // last view row's loads (W + 2r + 3 past its start)
+            const uint64_t rows = static_cast<uint64_t>(P->gy - 2 * P->r);
+            P->storage.row_pitch = P->fold_w;
+            P->storage.plane_pitch = rows * P->fold_w;
+            const uint64_t cells = std::max<uint64_t>(lp + P->fold_n, rows * P->fold_w + lp + 2 * P->r + 4);
+            P->storage.bytes = (cells + 3) / 4 * 4 * 4;
+        }
 
         ck(cudaMalloc(&P->d_a, P->img.a_smem.size() * 2), "cudaMalloc");
         ck(cudaMemcpy(P->d_a, P->img.a_smem.data(), P->img.a_smem.size() * 2, cudaMemcpyHostToDevice),
@@ -652,9 +706,10 @@ static void copy_dense(sst_plan* plan, int which, const float* src, float* dst, 
                        bool other_on_device, cudaStream_t st) {
     if (which < 0 || which > 1) throw std::invalid_argument("buffer index must be 0 or 1");
     if (!plan->buf[0]) throw std::invalid_argument("plan has no bound buffers");
-    const size_t w = static_cast<size_t>(plan->gx) * 4;
-    const size_t rows = static_cast<size_t>(plan->gy) * static_cast<size_t>(plan->gz);
-    const size_t pitch = plan->storage.row_pitch * 4;
+    const bool fold = plan->fold_n != 0;  // 1D: one contiguous row of fold_n cells
+    const size_t w = (fold ? static_cast<size_t>(plan->fold_n) : static_cast<size_t>(plan->gx)) * 4;
+    const size_t rows = fold ? 1 : static_cast<size_t>(plan->gy) * static_cast<size_t>(plan->gz);
+    const size_t pitch = fold ? w : plan->storage.row_pitch * 4;
     float* base = plan->buf[which] + plan->storage.left_pad;
     if (to_storage) {
         ck(cudaMemcpy2DAsync(base, pitch, src, w, w, rows,

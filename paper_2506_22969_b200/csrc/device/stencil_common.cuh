@@ -40,6 +40,7 @@ struct StepParams {
     int64_t row_pitch, plane_pitch;  // storage pitches (elements)
     int32_t left_pad;
     int32_t load_x0;           // storage column of the patch start relative to X0 (16B aligned)
+    int32_t load_y0;           // patch row offset: 0, or -r for a 1D fold's view (no ring rows)
     int32_t gx, gy, gz;        // logical extents
     int32_t r;                 // radius
     int32_t slow_lo, slow_hi;  // window over the slowest axis (y in 2D, z in 3D), interior coords

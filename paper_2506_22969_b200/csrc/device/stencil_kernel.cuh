@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_arrive_expect_tx(&patch_full[s], pbytes);
                     void* dst = sP + s * L.p_stride;
                     if (DIMS == 2)
-                        tma_load_2d(dst, &maps.in[p.src & 1], &patch_full[s], X0 + p.load_x0, Y0);
+                        tma_load_2d(dst, &maps.in[p.src & 1], &patch_full[s], X0 + p.load_x0, Y0 + p.load_y0);
                     else
                         tma_load_3d(dst, &maps.in[p.src & 1], &patch_full[s], X0 + p.load_x0, Y0, Z0);
                 }
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 void* dst = sP + s * L.p_stride;
                 const CUtensorMap* tin = &maps.in[(p.src + t) & 1];
                 if (DIMS == 2)
-                    tma_load_2d(dst, tin, &patch_full[s], X0 + p.load_x0, Y0);
+                    tma_load_2d(dst, tin, &patch_full[s], X0 + p.load_x0, Y0 + p.load_y0);
                 else
                     tma_load_3d(dst, tin, &patch_full[s], X0 + p.load_x0, Y0, Z0);
             }

@@ -26,6 +26,7 @@ struct sst_compiled {
     stensor::Sparse24Matrix a2;
     std::vector<std::uint64_t> col_origin_u64;
     std::uint64_t fuse = 1;
+    std::uint64_t fold_n = 0, fold_w = 0;  // 1D grid folded into a 2D view (device layout)
 };
 
 namespace sstc {
@@ -103,6 +104,26 @@ sst_status sst_compile(const char* stencil, const uint64_t* grid_dims, int ndims
         if (ndims != c->spec.dims || !grid_dims)
             throw std::invalid_argument("grid dimensionality does not match stencil");
         c->dims.assign(grid_dims, grid_dims + ndims);
+        if (c->spec.dims == 1 && r1 == 16 && r2 == 8) {
+            // 1D on the device layout: fold the grid into a 2D view (rows of W interior
+            // cells, W a multiple of the 128-wide batch) and embed the stencil as a 2D
+            // star stencil along the rows; the kernel's patch rows overlap by the halo,
+            // so the 1D neighbourhood of every cell is one view row.
+            const std::size_t N = c->dims[0], k = static_cast<std::size_t>(c->spec.k), r = (k - 1) / 2;
+            if (N < k) throw std::invalid_argument("grid smaller than kernel");
+            const std::size_t n_int = N - 2 * r;
+            const std::size_t W = std::min<std::size_t>(8192, (n_int + 127) / 128 * 128);
+            const std::size_t R = (n_int + W - 1) / W;
+            stensor::StencilSpec s2 = c->spec;
+            s2.dims = 2;
+            s2.shape = stensor::StencilShape::star;
+            for (auto& pt : s2.points) pt.off = {0, pt.off[0], 0};
+            stensor::validate(s2);
+            c->spec = s2;
+            c->dims = {R + 2 * r, W + 2 * r};
+            c->fold_n = N;
+            c->fold_w = W;
+        }
         if (r1 <= 0 || r2 <= 0) {
             const auto ex = stensor::explore_layouts_tcgen05(stensor::hw_preset("b200-sparse"),
                                                              c->spec, c->dims, 128);
@@ -149,6 +170,8 @@ sst_status sst_compiled_info(const sst_compiled* c, sst_compile_info* info) {
         info->window_h = L.stair.block_count;
         info->window_d = L.z_factor;
         for (std::size_t a = 0; a < c->dims.size() && a < 3; ++a) info->grid_dims[a] = c->dims[a];
+        info->fold_n = c->fold_n;
+        info->fold_w = c->fold_w;
         return SST_OK;
     } catch (...) {
         return sstc::from_current_exception();
@@ -216,6 +239,8 @@ sst_status sst_compiled_plan_desc(const sst_compiled* c, sst_plan_desc* d) {
         d->window_d = L.z_factor;
         d->precision = SST_PREC_F16;
         d->fuse = static_cast<uint32_t>(c->fuse);
+        d->fold_n = c->fold_n;
+        d->fold_w = c->fold_w;
         return SST_OK;
     } catch (...) {
         return sstc::from_current_exception();

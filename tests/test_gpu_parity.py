@@ -310,3 +310,43 @@ def test_f16x2_rejects_weights_not_exact_in_binary16(gpu):
     with pytest.raises(ValueError):
         SparseStencil(doc, [64, 64], precision="f16x2")
     SparseStencil(doc, [64, 64], precision="f16").close()  # f16 rounds A'' and is accepted
+
+
+# ---- 1D presets: the 1D grid folded into a 2D view (rows of W cells overlapping by
+# the halo, stencil embedded as a 2D star stencil along the rows; sst_compile)
+PRESETS_1D = ["Heat-1D", "1D5P"]
+
+
+@pytest.mark.parametrize("name", PRESETS_1D)
+@pytest.mark.parametrize("n", [5, 9, 129, 301, 8192 + 2, 100003, (1 << 20) + 7])
+def test_1d_one_step_bit_exact(gpu, name, n):
+    g = oracle.random_grid((n,), seed=8)
+    got, _ = run(name, g, 1)
+    assert np.array_equal(got, oracle.direct_apply(name, g, 1))
+
+
+@pytest.mark.parametrize("name,n,steps", [("Heat-1D", 70001, 40), ("1D5P", 20000, 25), ("Heat-1D", 9000, 100)])
+def test_1d_multi_step(gpu, name, n, steps):
+    g = oracle.random_grid((n,), seed=9)
+    got, _ = run(name, g, steps)
+    want = oracle.direct_apply(name, g, steps)
+    assert np.abs(got - want).max() <= tol_abs(steps)
+    cur = g  # exact round16 semantics per step, as for 2D/3D
+    for _ in range(steps):
+        cur = oracle.direct_apply(name, cur.astype(np.float16).astype(np.float64), 1)
+        cur = cur.astype(np.float32).astype(np.float64)
+    ulp = np.spacing(np.abs(cur).astype(np.float32)).astype(np.float64)
+    assert np.all(np.abs(got - cur) <= ulp), np.abs(got - cur).max()
+
+
+def test_1d_ring_kept_and_sparse_apply(gpu):
+    n, steps = 5000, 7
+    g = oracle.random_grid((n,), seed=10).astype(np.float32)
+    eng = SparseStencil("1D5P", [n])
+    try:
+        full = eng.apply_host(g, steps)
+    finally:
+        eng.close()
+    assert np.array_equal(full[:2], g[:2]) and np.array_equal(full[-2:], g[-2:])  # the ring keeps the input
+    out = sparse_apply("Heat-1D", g.astype(np.float64), 3)
+    assert out.shape == (n - 6,)
