@@ -157,7 +157,7 @@ int cmd_run(const Args& a) {
     const std::string text = stensor::is_preset(st) ? st : slurp(st);
     std::vector<uint64_t> d(dims.begin(), dims.end());
     sst_compiled* c = nullptr;
-    ck(sst_compile(text.c_str(), d.data(), static_cast<int>(d.size()), 0, 0, fuse, &c));
+    ck(sst_compile(text.c_str(), d.data(), static_cast<int>(d.size()), 16, 8, fuse, &c));  // device layout (1D: folded)
     sst_plan_desc desc;
     ck(sst_compiled_plan_desc(c, &desc));
     sst_plan* p = nullptr;

@@ -75,7 +75,9 @@ def test_verify_all_presets(gpu):
 
 
 @pytest.mark.gpu
-def test_run_time_loop(gpu):
-    r = sst("run", "--stencil", "Box-2D9P", "--grid", "2048x2048", "--steps", "50")
+@pytest.mark.parametrize("stencil,grid", [("Box-2D9P", "2048x2048"), ("Heat-1D", "1000000"),
+                                          ("Heat-3D", "64x64x64")])
+def test_run_time_loop(gpu, stencil, grid):
+    r = sst("run", "--stencil", stencil, "--grid", grid, "--steps", "50")
     assert r.returncode == 0, r.stderr
     assert "GStencil/s" in r.stdout and "launches" in r.stdout
