@@ -173,6 +173,7 @@ const Variant* variants(int& n) {
         make_stream_variant<4, 6, 3, true, 4, 8, 2>(), make_stream_variant<4, 4, 3, true, 4, 8, 2>(),
         make_stream_variant<4, 6, 3, true, 6, 8, 2>(), make_stream_variant<4, 4, 3, true, 4, 8, 1>(),
         make_stream_variant<4, 4, 3, true, 2, 8, 1>(), make_stream_variant<8, 3, 3, true, 3, 5, 1>(),
+        make_stream_variant<8, 2, 3, true, 2, 5, 2>(), make_stream_variant<8, 2, 3, true, 2, 4, 2>(),
         // 3D whole-window kernel (kz != 3 or non-streamable layouts): 25-27
         make_variant<3, 2, 4, false>(), make_variant<3, 2, 3, false>(), make_variant<3, 2, 2, false>(),
     };
