@@ -230,7 +230,7 @@ def run_engine(args, cfg, cfg_name):
     from paper_2506_22969_b200.multigpu import SlabStencil
 
     eng = SlabStencil(stencil, dims, rank=rank, world=ws, device=local, fuse=args.fuse,
-                      precision=args.precision)
+                      precision=args.precision, halo=args.halo)
     grid = eng.make_local_input(seed=1)  # dense fp32 torch tensor on the device
     eng.load(grid)
     stream = torch.cuda.current_stream(dev)
@@ -341,7 +341,7 @@ def run_engine(args, cfg, cfg_name):
                    "l2": ("L2 flushed (256 MB write, then 256 MB read) before every timed operator application, "
                           "outside the timed events") if flush is not None
                          else "inputs larger than L2 (ping-pong pair > 126 MB)",
-                   "parallelism": f"slab{ws}" if ws > 1 else "single GPU"},
+                   "parallelism": (f"slab{ws} ({args.halo} halos)" if ws > 1 else "single GPU")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
@@ -372,6 +372,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--halo", default="nccl", choices=["nccl", "p2p"],
+                    help="multi-GPU halo exchange: NCCL p2p overlapped with the interior window, or fused "
+                         "into the kernel (boundary slices stored into the neighbours' buffers over NVLink)")
     ap.add_argument("--precision", default="f16", choices=["f16", "f16x2"],
                     help="operand precision: f16 (round16 operands) or f16x2 (split hi+lo operand, ~fp32)")
     ap.add_argument("--fuse", type=int, default=1,

@@ -174,6 +174,32 @@ SST_API sst_status sst_run_steps(sst_plan* plan, int src, uint64_t steps, void* 
  * blocked axis (used by the multi-GPU driver to split interior / boundary
  * work); y1 <= y0 resets to the full interior. */
 SST_API sst_status sst_set_row_window(sst_plan* plan, uint64_t y0, uint64_t y1);
+/* ---- slab decomposition with peer-to-peer halos (fused halo exchange) ----
+ * sst_plan_set_peer(plan, 0, ...) names the upper neighbour (the rank holding the
+ * preceding slices of the slowest axis), 1 the lower one: its two ping-pong
+ * buffers (this process's mapping, e.g. from sst_ipc_open, over NVLink) and its
+ * slab size in slices (including its halo slices). From then on every step also
+ * stores this rank's first / last r interior slices straight into the
+ * neighbours' halo slices of the output parity (the same staged TMA boxes, tile by
+ * tile: no separate exchange). Ordering between ranks is the caller's: a rank may
+ * start step t + 1 once both neighbours finished step t (sst_stream_write_u32 /
+ * sst_stream_wait_geq_u32 on shared flags keep that on the streams).
+ * NULL buffers remove a peer. Not for 1D folds. */
+SST_API sst_status sst_plan_set_peer(sst_plan* plan, int which, void* buf0, void* buf1, uint64_t peer_slices);
+/* The plan's own ping-pong allocations (after sst_plan_bind(plan, NULL, NULL)):
+ * what sst_plan_set_peer expects of a neighbour (and what to export by IPC). */
+SST_API sst_status sst_plan_buffers(const sst_plan* plan, void** buf0, void** buf1);
+/* Zero-initialised device allocation (IPC-exportable, unlike sub-allocations). */
+SST_API sst_status sst_device_alloc(int device, size_t bytes, void** ptr);
+SST_API sst_status sst_device_free(void* ptr);
+/* CUDA IPC of a device allocation between the ranks of one node. */
+SST_API sst_status sst_ipc_handle(void* dev_ptr, uint8_t handle[64]);
+SST_API sst_status sst_ipc_open(int device, const uint8_t handle[64], void** dev_ptr);
+SST_API sst_status sst_ipc_close(void* dev_ptr);
+/* Stream-ordered flag write / wait (cuStreamWriteValue32 / cuStreamWaitValue32 GEQ). */
+SST_API sst_status sst_stream_write_u32(void* stream, uint32_t* dev_addr, uint32_t value);
+SST_API sst_status sst_stream_wait_geq_u32(void* stream, uint32_t* dev_addr, uint32_t value);
+
 /* Profiling aid: when dev_buf (device memory, 4 x u64 per CTA) is non-NULL,
  * every following launch writes per CTA {smid, start ns, main-loop start ns,
  * end ns} (globaltimer) at dev_buf[4 * cta]. NULL turns it off. */

@@ -25,6 +25,8 @@ EXPORTED = [
     "sst_set_row_window", "sst_plan_set_trace", "sst_apply_host", "sst_random_grid", "sst_last_error",
     "sst_device_count", "sst_version", "sst_run_compile", "sst_compile_result_destroy",
     "sst_compile_result_summary", "sst_compile_result_report", "sst_compile_result_lut", "sst_explore",
+    "sst_plan_set_peer", "sst_plan_buffers", "sst_device_alloc", "sst_device_free", "sst_ipc_handle",
+    "sst_ipc_open", "sst_ipc_close", "sst_stream_write_u32", "sst_stream_wait_geq_u32",
 ]
 
 
@@ -149,6 +151,15 @@ def lib() -> C.CDLL:
         "sst_compile_result_report": (i32, [P, P, sz, C.POINTER(sz)]),
         "sst_compile_result_lut": (i32, [P, P, sz, C.POINTER(sz)]),
         "sst_explore": (i32, [C.c_char_p, C.POINTER(u64), i32, C.c_char_p, u64, i32, P, sz, C.POINTER(sz)]),
+        "sst_plan_set_peer": (i32, [P, i32, P, P, u64]),
+        "sst_plan_buffers": (i32, [P, C.POINTER(P), C.POINTER(P)]),
+        "sst_device_alloc": (i32, [i32, sz, C.POINTER(P)]),
+        "sst_device_free": (i32, [P]),
+        "sst_ipc_handle": (i32, [P, C.POINTER(C.c_uint8)]),
+        "sst_ipc_open": (i32, [i32, C.POINTER(C.c_uint8), C.POINTER(P)]),
+        "sst_ipc_close": (i32, [P]),
+        "sst_stream_write_u32": (i32, [P, P, C.c_uint32]),
+        "sst_stream_wait_geq_u32": (i32, [P, P, C.c_uint32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

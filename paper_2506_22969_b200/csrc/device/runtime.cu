@@ -203,6 +203,12 @@ struct sst_plan {
     // ping-pong storage
     float* buf[2] = {nullptr, nullptr};
     bool owns_buf = false;
+    float* alloc_base[2] = {nullptr, nullptr};  // owned buffers: allocation start (guard rows first)
+    // owned 2D buffers start with kGuardRows rows that nothing reads: a lower
+    // neighbour's halo stores may start up to a box height above its halo rows
+    // (TMA store boxes cannot start at negative coordinates)
+    static constexpr int64_t kGuardRows = 64;
+    int64_t guard_elems() const { return dims == 2 ? kGuardRows * static_cast<int64_t>(storage.row_pitch) : 0; }
     sst::MapSet maps{};       // in[i]: patch loads over buffer i (whole storage);
                               // out[i]: stores into buffer i, clipped to the interior (and row window)
     uint32_t* d_sched = nullptr;  // dynamic batch counter of single-step 2D launches
@@ -218,6 +224,9 @@ struct sst_plan {
     uint64_t fuse = 1;   // original time steps per launch
     int load_x0 = 0;     // storage column of a batch's patch start, relative to X0
     uint64_t fold_n = 0, fold_w = 0;  // 1D grid folded into the 2D view (see sst_compile)
+    // slab P2P halos (sst_plan_set_peer): neighbour buffers by parity and slab size
+    float* peer_buf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [0 up, 1 down][parity]
+    uint64_t peer_slices[2] = {0, 0};
     float* d_ring_save = nullptr;     // fold: the r right-ring cells, restored after a run
 
     ~sst_plan() {
@@ -230,8 +239,8 @@ struct sst_plan {
         cudaFree(d_sched);
         cudaFree(d_ring_save);
         if (owns_buf) {
-            cudaFree(buf[0]);
-            cudaFree(buf[1]);
+            cudaFree(alloc_base[0]);
+            cudaFree(alloc_base[1]);
         }
     }
 
@@ -326,6 +335,28 @@ struct sst_plan {
                 const cuuint32_t rbox[3] = {4u, static_cast<cuuint32_t>(tiles_y * sst::kTileH), 1u};
                 encode(&maps.ring[i], 3, buf[i], gdim, gstride, rbox, CU_TENSOR_MAP_SWIZZLE_NONE);
             }
+            // neighbours' halo slices: the upper neighbour's last r slices receive this
+            // rank's interior slices [0, r) (coordinates as for the local map); the
+            // lower neighbour's first r slices receive [n_int - r, n_int) (the kernel
+            // subtracts peer_down0 from the slow coordinate)
+            const int64_t slice_pitch = dims == 3 ? static_cast<int64_t>(storage.plane_pitch)
+                                                  : static_cast<int64_t>(storage.row_pitch);
+            const int64_t inner0 = (dims == 3 ? r * static_cast<int64_t>(storage.row_pitch) : 0) +
+                                   static_cast<int64_t>(storage.left_pad) + r;
+            for (int w = 0; w < 2; ++w) {
+                if (!peer_buf[w][i]) continue;
+                // (2D lower peer: the map starts kGuardRows rows early, in its guard)
+                const int64_t guard = (w == 1 && dims == 2) ? kGuardRows : 0;
+                const int64_t first = w == 0 ? static_cast<int64_t>(peer_slices[0]) - r : -guard;  // peer slice
+                float* pbase = peer_buf[w][i] + first * slice_pitch + inner0;
+                cuuint64_t pdim[3] = {odim[0], odim[1], odim[2]};
+                if (dims == 2)
+                    pdim[1] = static_cast<cuuint64_t>(r + guard);
+                else
+                    pdim[2] = static_cast<cuuint64_t>(r);
+                encode(w == 0 ? &maps.peer_up[i] : &maps.peer_down[i], dims, pbase, pdim, gstride, obox,
+                       CU_TENSOR_MAP_SWIZZLE_128B);
+            }
         }
         map_lo = lo;
         map_hi = hi;
@@ -374,6 +405,18 @@ struct sst_plan {
         p.zchunk = zchunk;
         p.lo_sweep0 = img.lo_sweep0;
         p.load_y0 = fold_n ? -r : 0;  // fold: view rows have no ring rows above them
+        {   // slab P2P halos
+            const int64_t n_int = (dims == 3 ? gz : gy) - 2 * r;
+            p.peer_mask = (peer_buf[0][0] ? 1 : 0) | (peer_buf[1][0] ? 2 : 0);
+            p.peer_down0 = static_cast<int32_t>(n_int - r);
+            p.peer_down_c0 = static_cast<int32_t>(n_int - r - (dims == 2 ? kGuardRows : 0));
+            p.peer_up_shift = static_cast<int64_t>(peer_slices[0]) - 2 * r;
+            p.peer_down_shift = -n_int;
+            for (int i = 0; i < 2; ++i) {
+                p.peer_up_buf[i] = peer_buf[0][i];
+                p.peer_down_buf[i] = peer_buf[1][i];
+            }
+        }
         p.trace = trace;
         return p;
     }
@@ -407,7 +450,8 @@ struct sst_plan {
         const bool full = !(y_hi > y_lo);
         // (a fold's view rows depend on the next row's first cells: outside the
         // multi-step kernel's 3 x 3 batch neighbourhood, so folds run per step)
-        const bool multi = ms_env && variant->multistep && full && nsteps > 1 && !fold_n;
+        const bool multi = ms_env && variant->multistep && full && nsteps > 1 && !fold_n && !peer_buf[0][0] &&
+                           !peer_buf[1][0];
         if (multi && flags_n < p.nbatch) {
             cudaFree(d_flags);
             d_flags = nullptr;
@@ -679,13 +723,20 @@ sst_status sst_plan_bind(sst_plan* plan, void* b0, void* b1) {
         if (!plan) throw std::invalid_argument("null plan");
         ck(cudaSetDevice(plan->device), "cudaSetDevice");
         if (plan->owns_buf) {
-            cudaFree(plan->buf[0]);
-            cudaFree(plan->buf[1]);
+            cudaFree(plan->alloc_base[0]);
+            cudaFree(plan->alloc_base[1]);
+            plan->alloc_base[0] = plan->alloc_base[1] = nullptr;
             plan->owns_buf = false;
         }
         if (!b0 && !b1) {
-            ck(cudaMalloc(&plan->buf[0], plan->storage.bytes), "cudaMalloc(grid)");
-            ck(cudaMalloc(&plan->buf[1], plan->storage.bytes), "cudaMalloc(grid)");
+            const size_t guard = static_cast<size_t>(plan->guard_elems()) * 4;
+            for (int i = 0; i < 2; ++i) {
+                void* a = nullptr;
+                ck(cudaMalloc(&a, plan->storage.bytes + guard), "cudaMalloc(grid)");
+                ck(cudaMemset(a, 0, guard), "cudaMemset(guard)");
+                plan->alloc_base[i] = static_cast<float*>(a);
+                plan->buf[i] = plan->alloc_base[i] + plan->guard_elems();
+            }
             plan->owns_buf = true;
         } else {
             if (!b0 || !b1) throw std::invalid_argument("bind needs two buffers (or none)");
@@ -756,6 +807,128 @@ sst_status sst_plan_set_trace(sst_plan* plan, void* dev_buf) {
     try {
         if (!plan) throw std::invalid_argument("null plan");
         plan->trace = static_cast<unsigned long long*>(dev_buf);
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_plan_set_peer(sst_plan* plan, int which, void* buf0, void* buf1, uint64_t peer_slices) {
+    try {
+        if (!plan) throw std::invalid_argument("null plan");
+        if (which != 0 && which != 1) throw std::invalid_argument("peer must be 0 (upper) or 1 (lower)");
+        if (plan->fold_n) throw std::invalid_argument("peers are not supported for a 1D fold");
+        if ((buf0 == nullptr) != (buf1 == nullptr)) throw std::invalid_argument("peer needs both buffers");
+        if (buf0 && peer_slices < static_cast<uint64_t>(2 * plan->r))
+            throw std::invalid_argument("peer slab smaller than its halos");
+        // peers are plan-owned allocations (sst_plan_buffers): skip their guard rows
+        plan->peer_buf[which][0] = buf0 ? static_cast<float*>(buf0) + plan->guard_elems() : nullptr;
+        plan->peer_buf[which][1] = buf1 ? static_cast<float*>(buf1) + plan->guard_elems() : nullptr;
+        plan->peer_slices[which] = buf0 ? peer_slices : 0;
+        if (plan->tmap_ok) plan->make_tmaps();
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_plan_buffers(const sst_plan* plan, void** buf0, void** buf1) {
+    try {
+        if (!plan || !buf0 || !buf1) throw std::invalid_argument("null argument");
+        if (!plan->owns_buf) throw std::invalid_argument("plan buffers are caller-owned");
+        *buf0 = plan->alloc_base[0];
+        *buf1 = plan->alloc_base[1];
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_device_alloc(int device, size_t bytes, void** ptr) {
+    try {
+        if (!ptr) throw std::invalid_argument("null argument");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        ck(cudaMalloc(ptr, bytes), "cudaMalloc");
+        ck(cudaMemset(*ptr, 0, bytes), "cudaMemset");
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_device_free(void* ptr) {
+    try {
+        ck(cudaFree(ptr), "cudaFree");
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_ipc_handle(void* dev_ptr, uint8_t handle[64]) {
+    try {
+        if (!dev_ptr || !handle) throw std::invalid_argument("null argument");
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+        cudaIpcMemHandle_t h;
+        ck(cudaIpcGetMemHandle(&h, dev_ptr), "cudaIpcGetMemHandle");
+        std::memcpy(handle, &h, 64);
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_ipc_open(int device, const uint8_t handle[64], void** dev_ptr) {
+    try {
+        if (!dev_ptr || !handle) throw std::invalid_argument("null argument");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, 64);
+        ck(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_ipc_close(void* dev_ptr) {
+    try {
+        ck(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+namespace {
+using StreamValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+StreamValueFn stream_fn(const char* name) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    ck(cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q), "cudaGetDriverEntryPoint");
+    if (!p || q != cudaDriverEntryPointSuccess) throw CudaError(std::string(name) + " unavailable", false);
+    return reinterpret_cast<StreamValueFn>(p);
+}
+}  // namespace
+
+sst_status sst_stream_write_u32(void* stream, uint32_t* dev_addr, uint32_t value) {
+    try {
+        static StreamValueFn fn = stream_fn("cuStreamWriteValue32");
+        const CUresult rc = fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(dev_addr), value,
+                               CU_STREAM_WRITE_VALUE_DEFAULT);
+        if (rc != CUDA_SUCCESS) throw CudaError("cuStreamWriteValue32 failed (" + std::to_string(rc) + ")", false);
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_stream_wait_geq_u32(void* stream, uint32_t* dev_addr, uint32_t value) {
+    try {
+        static StreamValueFn fn = stream_fn("cuStreamWaitValue32");
+        const CUresult rc = fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(dev_addr), value,
+                               CU_STREAM_WAIT_VALUE_GEQ);
+        if (rc != CUDA_SUCCESS) throw CudaError("cuStreamWaitValue32 failed (" + std::to_string(rc) + ")", false);
         return SST_OK;
     } catch (...) {
         return sstc::from_current_exception();

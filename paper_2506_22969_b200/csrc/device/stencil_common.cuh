@@ -25,6 +25,10 @@ struct MapSet {
     CUtensorMap in[2];
     CUtensorMap out[2];
     CUtensorMap ring[2];  // 3D stream kernel: {4, TYB*8, 1} boxes of the right-edge chunk (kEdgeRing)
+    // slab decomposition with peer-to-peer halos: the neighbours' halo slices in
+    // their buffers (by output parity), addressed in this rank's interior coordinates
+    CUtensorMap peer_up[2];
+    CUtensorMap peer_down[2];
 };
 
 struct StepParams {
@@ -55,6 +59,13 @@ struct StepParams {
     int32_t tmem_cols;         // TMEM allocation (power of two >= the kernel's column budget)
     int32_t zchunk;            // 3D stream kernel: output planes per (band, z-chunk) run; 0 = whole column
     int32_t lo_sweep0;         // first gather sweep writing B_lo rows (SST_PREC_F16X2); = k_pad/32 otherwise
+    int32_t peer_mask;         // slab P2P halos: 1 = upper neighbour (lower slices), 2 = lower neighbour
+    int32_t peer_down0;        // first interior slice that is the lower neighbour's halo (n_int - r)
+    int32_t peer_down_c0;      // slice coordinate origin of the lower neighbour's map (>= 0 coordinates)
+    int64_t peer_up_shift;     // (2D plain edge stores) storage-row shift into the upper neighbour's buffer
+    int64_t peer_down_shift;   // ... into the lower neighbour's buffer
+    float* peer_up_buf[2];     // neighbours' buffers by parity (plain right-edge stores)
+    float* peer_down_buf[2];
     uint32_t* sched;           // 2D single-step launches: global batch counter (dynamic scheduling), or null
     uint32_t sched_base;       // counter value at launch start
     unsigned long long* trace; // profiling only (sst_plan_set_trace): per CTA {smid, t_start, t_main, t_end}
@@ -271,7 +282,8 @@ __device__ __forceinline__ void tmem_load_batch(uint32_t taddr, uint32_t (&v)[kT
 template <int DIMS, int TYB>
 __device__ __forceinline__ void store_right_edge(const StepParams& p, float* dst,
                                                  const uint32_t (&v)[kTXB / 2][2 * TYB], int X0, int Y0,
-                                                 int Z0, uint32_t q, uint32_t lane) {
+                                                 int Z0, uint32_t q, uint32_t lane, float* peer_up = nullptr,
+                                                 float* peer_down = nullptr) {
     constexpr int NBOX = kTXB / 2;
     const int ox = p.gx - 2 * p.r, ox4 = ox & ~3;
     if (X0 + kTXB * kTileW <= ox4 || (p.debug_mode & 8)) return;
@@ -289,8 +301,19 @@ __device__ __forceinline__ void store_right_edge(const StepParams& p, float* dst
             const int xr = X0 + xo + dxl;
             if (xr >= ox4 && xr < ox) {
 #pragma unroll
-                for (int ty = 0; ty < TYB; ++ty)
-                    if (y0 + ty * kTileH < y_lim) rowp[xo + ty * ystep] = __uint_as_float(v[c][2 * ty + par]);
+                for (int ty = 0; ty < TYB; ++ty) {
+                    const int y = y0 + ty * kTileH;
+                    if (y >= y_lim) continue;
+                    const float val = __uint_as_float(v[c][2 * ty + par]);
+                    rowp[xo + ty * ystep] = val;
+                    if constexpr (DIMS == 2) {  // slab P2P halos: the neighbours' copies
+                        const int64_t off = static_cast<int64_t>(y + p.r) * p.row_pitch + p.left_pad + p.r + X0 + dxl + xo;
+                        if ((p.peer_mask & 1) && y < p.r)
+                            peer_up[off + p.peer_up_shift * p.row_pitch] = val;
+                        if ((p.peer_mask & 2) && y >= p.peer_down0)
+                            peer_down[off + p.peer_down_shift * p.row_pitch] = val;
+                    }
+                }
             }
         }
 }
@@ -311,7 +334,10 @@ template <int DIMS, int TYB, int NS, int EDGE = kEdgePlain>
 __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorMap* tmap_out, float* dst,
                                             uint32_t (&v)[kTXB / 2][2 * TYB], uint8_t* sS,
                                             uint32_t s_stride, int nb, int X0, int Y0, int Z0,
-                                            uint32_t q, uint32_t lane, int etid, const float* ring = nullptr) {
+                                            uint32_t q, uint32_t lane, int etid, const float* ring = nullptr,
+                                            const CUtensorMap* peer_up = nullptr,
+                                            const CUtensorMap* peer_down = nullptr, float* peer_up_buf = nullptr,
+                                            float* peer_down_buf = nullptr) {
     using namespace ptx;
     constexpr int CW = 2 * TYB, NBOX = kTXB / 2;
     const uint32_t dy = lane % 8, w4 = (lane / 8) * 4;
@@ -319,7 +345,7 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
     // last column the store map covers (exclusive)
     const int oxs = (EDGE == kEdgeRing && ox4 != ox) ? ox4 + 4 : ox4;
     if constexpr (EDGE == kEdgePlain) {
-        store_right_edge<DIMS, TYB>(p, dst, v, X0, Y0, Z0, q, lane);
+        store_right_edge<DIMS, TYB>(p, dst, v, X0, Y0, Z0, q, lane, peer_up_buf, peer_down_buf);
     } else {
         if (ring != nullptr && X0 + kTXB * kTileW > ox) {
             const int dxl = static_cast<int>(q) * 4 + static_cast<int>(lane / 8);
@@ -368,6 +394,32 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
                 tma_store_2d(tmap_out, sS + buf + c * s_stride, bx0, Y0 - p.slow_lo);  // map starts at the window
             else
                 tma_store_3d(tmap_out, sS + buf + c * s_stride, bx0, Y0, Z0);
+        }
+        // slab decomposition with peer-to-peer halos: boundary slices also go straight
+        // into the neighbours' halo slices (NVLink stores of the same staged boxes;
+        // the peer maps span only the r halo slices, TMA clips everything else)
+        const int slice0 = DIMS == 2 ? Y0 : Z0, nslice = DIMS == 2 ? TYB * kTileH : 1;
+        if (peer_up != nullptr && slice0 < p.r) {
+#pragma unroll
+            for (int c = 0; c < NBOX; ++c) {
+                const int bx0 = X0 + c * kBoxW;
+                if (bx0 >= oxs) break;
+                if (DIMS == 2)
+                    tma_store_2d(peer_up, sS + buf + c * s_stride, bx0, Y0);
+                else
+                    tma_store_3d(peer_up, sS + buf + c * s_stride, bx0, Y0, Z0);
+            }
+        }
+        if (peer_down != nullptr && slice0 + nslice > p.peer_down0) {
+#pragma unroll
+            for (int c = 0; c < NBOX; ++c) {
+                const int bx0 = X0 + c * kBoxW;
+                if (bx0 >= oxs) break;
+                if (DIMS == 2)
+                    tma_store_2d(peer_down, sS + buf + c * s_stride, bx0, Y0 - p.peer_down_c0);
+                else
+                    tma_store_3d(peer_down, sS + buf + c * s_stride, bx0, Y0, Z0 - p.peer_down_c0);
+            }
         }
         bulk_commit();
     }

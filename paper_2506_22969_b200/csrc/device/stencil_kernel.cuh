@@ -433,8 +433,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (lane == 0) mbar_arrive(&d_empty[s]);
             }
             if (!(p.debug_mode & 1))
-                store_batch<DIMS, TYB, kStageBufs>(p, &maps.out[(p.src + t + 1) & 1], buf_of(p, p.src + t + 1),
-                                                   v, sS, L.s_stride, r - 1, X0, Y0, Z0, q, lane, etid);
+            {
+                const int par = (p.src + t + 1) & 1;
+                store_batch<DIMS, TYB, kStageBufs>(
+                    p, &maps.out[par], buf_of(p, par), v, sS, L.s_stride, r - 1, X0, Y0, Z0, q, lane, etid,
+                    nullptr, (p.peer_mask & 1) ? &maps.peer_up[par] : nullptr,
+                    (p.peer_mask & 2) ? &maps.peer_down[par] : nullptr, par ? p.peer_up_buf[1] : p.peer_up_buf[0],
+                    par ? p.peer_down_buf[1] : p.peer_down_buf[0]);
+            }
             committed = j + 1;
             if (multi && etid == 0 && committed - published >= PUB_EVERY + PUB_LAG) {
                 bulk_wait<PUB_LAG>();

@@ -13,6 +13,13 @@ compute is the engine's sm_100a kernel restricted to a slice window
 (sst_set_row_window); the exchange is pure plumbing on views of the plan's
 ping-pong buffers. With world == 1 a step is a single full-interior launch.
 
+halo="p2p" fuses the exchange into the compute instead: the ranks map each
+other's buffers (CUDA IPC; NVLink peer memory on a node) and every step's
+epilogue stores the first / last r interior slices into the neighbours' halo
+slices as part of its own TMA stores (sst_plan_set_peer). One launch per step,
+no exchange step; neighbours are ordered on the streams by flag words
+(cuStreamWriteValue32 after a step, cuStreamWaitValue32 before the next).
+
 The index bookkeeping (which slices a rank owns, sends and receives) lives in
 `SlabLayout` so it is testable without a GPU (tests/test_multigpu.py runs it
 over gloo with world_size 2).
@@ -149,7 +156,10 @@ class SlabStencil:
     """A rank's share of a slab-decomposed stencil sweep on its B200."""
 
     def __init__(self, stencil: str, dims_per_rank: Sequence[int], rank: int = 0, world: int = 1,
-                 device: int = 0, group=None, fuse: int = 1, precision: str = "f16"):
+                 device: int = 0, group=None, fuse: int = 1, precision: str = "f16", halo: str = "nccl"):
+        if halo not in ("nccl", "p2p"):
+            raise ValueError("halo must be 'nccl' or 'p2p'")
+        self.halo = halo
         import torch
 
         from .engine import Compiled, SparseStencil
@@ -165,11 +175,91 @@ class SlabStencil:
         self.device = device
         self.group = group
         self.eng = SparseStencil(stencil, self.local_dims, device=device, fuse=self.fuse, precision=precision)
-        self.bufs = self.eng.bind_torch()
-        self.flat = [b.view(torch.float32) for b in self.bufs]
+        self._peers_open = []
+        self._flags = None
+        if halo == "p2p" and world > 1:
+            self.eng.bind()  # plan-owned allocations: IPC-exportable as a whole
+            self._setup_p2p()
+            self.bufs = None
+            self.flat = None
+        else:
+            self.bufs = self.eng.bind_torch()
+            self.flat = [b.view(torch.float32) for b in self.bufs]
         st = self.eng.storage
         self.pitch = int(st["plane_pitch"] if len(self.local_dims) == 3 else st["row_pitch"])
         self.cur = 0
+
+    # -- P2P halos ---------------------------------------------------------
+    def _setup_p2p(self):
+        """Exchange IPC handles of both ping-pong buffers and a flag pair per rank;
+        map the neighbours' and register them as the plan's peers."""
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        from ._capi import check, lib
+
+        L = lib()
+        b0, b1 = C.c_void_p(), C.c_void_p()
+        check(L.sst_plan_buffers(self.eng._h, C.byref(b0), C.byref(b1)))
+        flags = C.c_void_p()  # uint32 [from_up, from_down]: launches the neighbour finished
+        check(L.sst_device_alloc(int(self.device), 8, C.byref(flags)))
+        self._flags = flags.value
+
+        def handle(ptr):
+            h = (C.c_uint8 * 64)()
+            check(L.sst_ipc_handle(C.c_void_p(ptr), h))
+            return bytes(h)
+
+        mine = {"bufs": [handle(b0.value), handle(b1.value)], "flags": handle(flags.value),
+                "slices": self.layout.local_slices}
+        table = [None] * self.layout.world
+        dist.all_gather_object(table, mine, group=self.group)
+
+        def open_(h):
+            p = C.c_void_p()
+            check(L.sst_ipc_open(int(self.device), (C.c_uint8 * 64).from_buffer_copy(h), C.byref(p)))
+            self._peers_open.append(p.value)
+            return p.value
+
+        self._peer_flag = {}
+        for which, nb in ((0, self.layout.rank - 1), (1, self.layout.rank + 1)):
+            if not 0 <= nb < self.layout.world:
+                continue
+            e = table[nb]
+            pb = [open_(e["bufs"][0]), open_(e["bufs"][1])]
+            check(L.sst_plan_set_peer(self.eng._h, which, C.c_void_p(pb[0]), C.c_void_p(pb[1]),
+                                      int(e["slices"])))
+            # my step count goes into the neighbour's slot that names me: I am the
+            # lower neighbour (from_down, +4) of my upper one and vice versa
+            self._peer_flag[which] = open_(e["flags"]) + (4 if which == 0 else 0)
+        self._launch = 0
+        dist.barrier(group=self.group)
+
+    def _p2p_fence(self):
+        """P2P halos: neighbours write into this rank's buffers from their first
+        step on, so every rank must have finished (re)loading before any steps."""
+        if self.halo == "p2p" and self.layout.world > 1:
+            import torch
+            import torch.distributed as dist
+
+            torch.cuda.synchronize(torch.device("cuda", self.device))
+            dist.barrier(group=self.group)
+
+    def _step_p2p(self, stream):
+        import ctypes as C
+
+        from ._capi import check, lib
+
+        L = lib()
+        u = self._launch
+        for which in self._peer_flag:  # both neighbours finished launch u - 1
+            check(L.sst_stream_wait_geq_u32(C.c_void_p(stream or None), C.c_void_p(self._flags + 4 * which),
+                                            u))
+        self.cur = self.eng.run(self.fuse, src=self.cur, stream=stream)
+        for which, addr in self._peer_flag.items():
+            check(L.sst_stream_write_u32(C.c_void_p(stream or None), C.c_void_p(addr), u + 1))
+        self._launch = u + 1
 
     # -- data --------------------------------------------------------------
     def make_local_input(self, seed: int = 1):
@@ -190,6 +280,7 @@ class SlabStencil:
 
     def load(self, grid):
         self.eng.upload(grid, which=0)
+        self._p2p_fence()
         self.cur = 0
 
     def result(self):
@@ -226,6 +317,11 @@ class SlabStencil:
             return
         if steps % self.fuse:
             raise ValueError("steps must be a multiple of the fusion factor")
+        if self.halo == "p2p":
+            self.eng.set_row_window(0, 0)
+            for _ in range(steps // self.fuse):
+                self._step_p2p(stream)
+            return
         for _ in range(steps // self.fuse):
             works = exchange_halos(self.layout, self.flat[self.cur], self.pitch, self.group)
             a, b = self.layout.interior_window()
@@ -246,6 +342,7 @@ class SlabStencil:
         import torch
 
         self.eng.upload(np.ascontiguousarray(host, dtype=np.float32), which=0)
+        self._p2p_fence()
         self.cur = 0
         self.step(steps)
         if out is None:
@@ -255,4 +352,18 @@ class SlabStencil:
         return out
 
     def close(self):
+        import ctypes as C
+
+        from ._capi import lib
+
+        if self._peers_open or self._flags:
+            import torch
+
+            torch.cuda.synchronize(torch.device("cuda", self.device))
+        for p in self._peers_open:
+            lib().sst_ipc_close(C.c_void_p(p))
+        self._peers_open = []
+        if self._flags:
+            lib().sst_device_free(C.c_void_p(self._flags))
+            self._flags = None
         self.eng.close()
