@@ -226,6 +226,8 @@ struct sst_plan {
     uint64_t fold_n = 0, fold_w = 0;  // 1D grid folded into the 2D view (see sst_compile)
     // slab P2P halos (sst_plan_set_peer): neighbour buffers by parity and slab size
     float* peer_buf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [0 up, 1 down][parity]
+    sst::PeerMaps peer_maps_h{};              // encoded here, copied to d_peer_maps
+    sst::PeerMaps* d_peer_maps = nullptr;
     uint64_t peer_slices[2] = {0, 0};
     float* d_ring_save = nullptr;     // fold: the r right-ring cells, restored after a run
 
@@ -238,6 +240,7 @@ struct sst_plan {
         cudaFree(d_flags);
         cudaFree(d_sched);
         cudaFree(d_ring_save);
+        cudaFree(d_peer_maps);
         if (owns_buf) {
             cudaFree(alloc_base[0]);
             cudaFree(alloc_base[1]);
@@ -354,9 +357,14 @@ struct sst_plan {
                     pdim[1] = static_cast<cuuint64_t>(r + guard);
                 else
                     pdim[2] = static_cast<cuuint64_t>(r);
-                encode(w == 0 ? &maps.peer_up[i] : &maps.peer_down[i], dims, pbase, pdim, gstride, obox,
+                encode(w == 0 ? &peer_maps_h.up[i] : &peer_maps_h.down[i], dims, pbase, pdim, gstride, obox,
                        CU_TENSOR_MAP_SWIZZLE_128B);
             }
+        }
+        if (peer_buf[0][0] || peer_buf[1][0]) {
+            if (!d_peer_maps) ck(cudaMalloc(&d_peer_maps, sizeof(sst::PeerMaps)), "cudaMalloc(peer maps)");
+            ck(cudaMemcpy(d_peer_maps, &peer_maps_h, sizeof(sst::PeerMaps), cudaMemcpyHostToDevice),
+               "cudaMemcpy(peer maps)");
         }
         map_lo = lo;
         map_hi = hi;
@@ -408,6 +416,7 @@ struct sst_plan {
         {   // slab P2P halos
             const int64_t n_int = (dims == 3 ? gz : gy) - 2 * r;
             p.peer_mask = (peer_buf[0][0] ? 1 : 0) | (peer_buf[1][0] ? 2 : 0);
+            p.peer_maps = d_peer_maps;
             p.peer_down0 = static_cast<int32_t>(n_int - r);
             p.peer_down_c0 = static_cast<int32_t>(n_int - r - (dims == 2 ? kGuardRows : 0));
             p.peer_up_shift = static_cast<int64_t>(peer_slices[0]) - 2 * r;

@@ -311,8 +311,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (!(p.debug_mode & 1))
                     store_batch<3, TYB, NS, kEdgeRing>(
                         p, tmap_out, buf_of(p, p.src ^ 1), v, sS, L.s_stride, o, X0, Y0, p.slow_lo + zo, q, lane,
-                        etid, ring, (p.peer_mask & 1) ? &maps.peer_up[p.src ^ 1] : nullptr,
-                        (p.peer_mask & 2) ? &maps.peer_down[p.src ^ 1] : nullptr);
+                        etid, ring, (p.peer_mask & 1) ? &p.peer_maps->up[p.src ^ 1] : nullptr,
+                        (p.peer_mask & 2) ? &p.peer_maps->down[p.src ^ 1] : nullptr);
             }
             it_base += zo_b - zo_a + 1 + 2 * R;
         });

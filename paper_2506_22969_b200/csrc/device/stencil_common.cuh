@@ -25,10 +25,15 @@ struct MapSet {
     CUtensorMap in[2];
     CUtensorMap out[2];
     CUtensorMap ring[2];  // 3D stream kernel: {4, TYB*8, 1} boxes of the right-edge chunk (kEdgeRing)
-    // slab decomposition with peer-to-peer halos: the neighbours' halo slices in
-    // their buffers (by output parity), addressed in this rank's interior coordinates
-    CUtensorMap peer_up[2];
-    CUtensorMap peer_down[2];
+};
+
+// Slab decomposition with peer-to-peer halos: the neighbours' halo slices in their
+// buffers (by output parity), addressed in this rank's interior coordinates. Kept in
+// global memory (TMA reads tensor maps from .global too) rather than in the kernel
+// parameters: a larger parameter block measurably slowed L2-cold launches.
+struct PeerMaps {
+    CUtensorMap up[2];
+    CUtensorMap down[2];
 };
 
 struct StepParams {
@@ -59,6 +64,7 @@ struct StepParams {
     int32_t tmem_cols;         // TMEM allocation (power of two >= the kernel's column budget)
     int32_t zchunk;            // 3D stream kernel: output planes per (band, z-chunk) run; 0 = whole column
     int32_t lo_sweep0;         // first gather sweep writing B_lo rows (SST_PREC_F16X2); = k_pad/32 otherwise
+    const PeerMaps* peer_maps; // slab P2P halos (device memory), or null
     int32_t peer_mask;         // slab P2P halos: 1 = upper neighbour (lower slices), 2 = lower neighbour
     int32_t peer_down0;        // first interior slice that is the lower neighbour's halo (n_int - r)
     int32_t peer_down_c0;      // slice coordinate origin of the lower neighbour's map (>= 0 coordinates)
@@ -282,8 +288,7 @@ __device__ __forceinline__ void tmem_load_batch(uint32_t taddr, uint32_t (&v)[kT
 template <int DIMS, int TYB>
 __device__ __forceinline__ void store_right_edge(const StepParams& p, float* dst,
                                                  const uint32_t (&v)[kTXB / 2][2 * TYB], int X0, int Y0,
-                                                 int Z0, uint32_t q, uint32_t lane, float* peer_up = nullptr,
-                                                 float* peer_down = nullptr) {
+                                                 int Z0, uint32_t q, uint32_t lane) {
     constexpr int NBOX = kTXB / 2;
     const int ox = p.gx - 2 * p.r, ox4 = ox & ~3;
     if (X0 + kTXB * kTileW <= ox4 || (p.debug_mode & 8)) return;
@@ -301,21 +306,36 @@ __device__ __forceinline__ void store_right_edge(const StepParams& p, float* dst
             const int xr = X0 + xo + dxl;
             if (xr >= ox4 && xr < ox) {
 #pragma unroll
-                for (int ty = 0; ty < TYB; ++ty) {
-                    const int y = y0 + ty * kTileH;
-                    if (y >= y_lim) continue;
-                    const float val = __uint_as_float(v[c][2 * ty + par]);
-                    rowp[xo + ty * ystep] = val;
-                    if constexpr (DIMS == 2) {  // slab P2P halos: the neighbours' copies
-                        const int64_t off = static_cast<int64_t>(y + p.r) * p.row_pitch + p.left_pad + p.r + X0 + dxl + xo;
-                        if ((p.peer_mask & 1) && y < p.r)
-                            peer_up[off + p.peer_up_shift * p.row_pitch] = val;
-                        if ((p.peer_mask & 2) && y >= p.peer_down0)
-                            peer_down[off + p.peer_down_shift * p.row_pitch] = val;
-                    }
-                }
+                for (int ty = 0; ty < TYB; ++ty)
+                    if (y0 + ty * kTileH < y_lim) rowp[xo + ty * ystep] = __uint_as_float(v[c][2 * ty + par]);
             }
         }
+}
+
+// Slab P2P halos, 2D: the <= 3 right-edge columns of the neighbours' halo rows
+// (TMA stores clip them). Rare (right-edge batches of the boundary bands), so one
+// warp copies them from the staged boxes after the staging barrier in a rolled loop
+// (reading registers instead would unroll the whole edge case again per peer).
+__device__ __forceinline__ void peer_right_edge(const StepParams& p, uint32_t stage, uint32_t s_stride, int X0,
+                                                int Y0, int rows, float* up, float* down, uint32_t lane) {
+    const int ox = p.gx - 2 * p.r, ox4 = ox & ~3;
+    if (X0 + kTXB * kTileW <= ox4 || ox4 == ox) return;
+    const int c = (ox4 - X0) / kBoxW;  // the box holding [ox4, ox4 + 4)
+    const int w = ox - ox4;
+    for (int e = static_cast<int>(lane); e < rows * w; e += 32) {
+        const int yl = e / w, x = ox4 + e % w, y = Y0 + yl;
+        const bool to_up = up != nullptr && y < p.r, to_down = down != nullptr && y >= p.peer_down0;
+        if (!(to_up || to_down) || y >= p.slow_hi) continue;
+        const int xl = x - X0 - c * kBoxW;
+        float val;
+        asm volatile("ld.shared.f32 %0, [%1];"
+                     : "=f"(val)
+                     : "r"(stage + static_cast<uint32_t>(c) * s_stride + static_cast<uint32_t>(yl) * 128u +
+                           (static_cast<uint32_t>((xl / 4) ^ (yl % 8)) * 16u) + static_cast<uint32_t>(xl % 4) * 4u));
+        const int64_t off = static_cast<int64_t>(y + p.r) * p.row_pitch + p.left_pad + p.r + x;
+        if (to_up) up[off + p.peer_up_shift * p.row_pitch] = val;
+        if (to_down) down[off + p.peer_down_shift * p.row_pitch] = val;
+    }
 }
 
 // Right-edge handling of store_batch:
@@ -345,7 +365,7 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
     // last column the store map covers (exclusive)
     const int oxs = (EDGE == kEdgeRing && ox4 != ox) ? ox4 + 4 : ox4;
     if constexpr (EDGE == kEdgePlain) {
-        store_right_edge<DIMS, TYB>(p, dst, v, X0, Y0, Z0, q, lane, peer_up_buf, peer_down_buf);
+        store_right_edge<DIMS, TYB>(p, dst, v, X0, Y0, Z0, q, lane);
     } else {
         if (ring != nullptr && X0 + kTXB * kTileW > ox) {
             const int dxl = static_cast<int>(q) * 4 + static_cast<int>(lane / 8);
@@ -384,6 +404,9 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
     // async-proxy (TMA) reads with one proxy fence. A per-thread fence right after the
     // stores instead costs each thread a MEMBAR over its 32-64 stores in flight.
     named_bar_sync(kEpiBarrier, kEpiWarps * 32);
+    if constexpr (DIMS == 2)
+        if (p.peer_mask != 0 && etid >= 32 && etid < 64 && (Y0 < p.r || Y0 + TYB * kTileH > p.peer_down0))
+            peer_right_edge(p, stage, s_stride, X0, Y0, TYB * kTileH, peer_up_buf, peer_down_buf, lane);
     if (etid == 0) {
         fence_proxy_async_smem();
 #pragma unroll
@@ -400,7 +423,7 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
         // the peer maps span only the r halo slices, TMA clips everything else)
         const int slice0 = DIMS == 2 ? Y0 : Z0, nslice = DIMS == 2 ? TYB * kTileH : 1;
         if (peer_up != nullptr && slice0 < p.r) {
-#pragma unroll
+#pragma unroll 1
             for (int c = 0; c < NBOX; ++c) {
                 const int bx0 = X0 + c * kBoxW;
                 if (bx0 >= oxs) break;
@@ -411,7 +434,7 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
             }
         }
         if (peer_down != nullptr && slice0 + nslice > p.peer_down0) {
-#pragma unroll
+#pragma unroll 1
             for (int c = 0; c < NBOX; ++c) {
                 const int bx0 = X0 + c * kBoxW;
                 if (bx0 >= oxs) break;

@@ -437,8 +437,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int par = (p.src + t + 1) & 1;
                 store_batch<DIMS, TYB, kStageBufs>(
                     p, &maps.out[par], buf_of(p, par), v, sS, L.s_stride, r - 1, X0, Y0, Z0, q, lane, etid,
-                    nullptr, (p.peer_mask & 1) ? &maps.peer_up[par] : nullptr,
-                    (p.peer_mask & 2) ? &maps.peer_down[par] : nullptr, par ? p.peer_up_buf[1] : p.peer_up_buf[0],
+                    nullptr, (p.peer_mask & 1) ? &p.peer_maps->up[par] : nullptr,
+                    (p.peer_mask & 2) ? &p.peer_maps->down[par] : nullptr, par ? p.peer_up_buf[1] : p.peer_up_buf[0],
                     par ? p.peer_down_buf[1] : p.peer_down_buf[0]);
             }
             committed = j + 1;
