@@ -116,14 +116,33 @@ Variant make_variant() {
     v.layout = [](int nks, int k_pad, int pw, int ph, int planes) {
         return sst::smem_layout<TYB, NP, AT>(nks, k_pad, pw, ph, planes);
     };
+    // 2D: one instantiation per time-loop mode (static / dynamic / multi-step)
     v.configure = [](int smem) {
-        ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT>,
+        ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeStatic>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
            "cudaFuncSetAttribute");
+        if constexpr (D == 2) {
+            ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeDynamic>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+               "cudaFuncSetAttribute");
+            ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMulti>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+               "cudaFuncSetAttribute");
+        }
     };
     v.multistep = D == 2;
     v.launch = [](int grid, int smem, cudaStream_t st, const sst::MapSet& maps, const sst::StepParams& p,
-                  bool coop) { launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT>, grid, smem, st, maps, p, coop); };
+                  bool coop) {
+        if constexpr (D == 2) {
+            if (p.nsteps > 1)
+                return launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMulti>, grid, smem, st, maps,
+                                  p, coop);
+            if (p.sched)
+                return launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeDynamic>, grid, smem, st,
+                                  maps, p, coop);
+        }
+        launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeStatic>, grid, smem, st, maps, p, coop);
+    };
     return v;
 }
 

@@ -119,7 +119,12 @@ __device__ __forceinline__ uint32_t refresh_min(const StepParams& p, uint32_t ne
 // after it loaded its step-t patch). CTAs walk batches in the same order every
 // step, so in steady state the flags are long set when checked: no per-step
 // launch, prologue or tail.
-template <int DIMS, int TYB, int NP, bool AT>
+// MODE (compile-time, so each launch runs only its own code path: the kernel's
+// instruction footprint matters for L2-cold launches): 0 static batch striding,
+// 1 dynamic batches (p.sched), 2 multi-step dataflow (p.nsteps > 1, p.flags).
+enum StepMode { kModeStatic = 0, kModeDynamic = 1, kModeMulti = 2 };
+
+template <int DIMS, int TYB, int NP, bool AT, int MODE = kModeStatic>
 __global__ void __launch_bounds__(kThreads, 1)
     stencil_step_kernel(const __grid_constant__ MapSet maps, const StepParams p) {
     constexpr int N = kTXB * TYB;
@@ -217,9 +222,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         Y0 = ((b / nbx) % nby) * (TYB * kTileH) + (DIMS == 2 ? p.slow_lo : 0);
         Z0 = b / (nbx * nby) + (DIMS == 3 ? p.slow_lo : 0);
     };
-    const bool multi = p.nsteps > 1;
+    constexpr bool multi = MODE == kModeMulti;
     // single-step launches with a scheduler counter draw batches dynamically
-    const bool dyn = p.sched != nullptr && !multi;
+    constexpr bool dyn = MODE == kModeDynamic;
     auto next_bid = [&](int r) {  // consumers: batch index of real iteration r (-1: done)
         mbar_wait(&bid_full[r % kBidSlots], (r / kBidSlots) & 1);
         return sBid[r % kBidSlots];
@@ -233,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t pbytes = static_cast<uint32_t>(p.patch_w * p.patch_h * p.patch_planes) * 4u;
         uint32_t polls = 0, known = p.flag_base;  // min over all progress counters seen
         int r = 0;                                // real (non no-op) iterations
-        if (dyn) {
+        if constexpr (dyn) {
             // a CTA's first batch is blockIdx.x, later ones G + counter draws; the
             // next index is drawn one batch ahead so the atomic's latency hides
             // behind the current batch's wait / issue
@@ -304,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int r = 0;
         for (int j = 0; dyn || j < total; ++j, ++r) {
             int t, b;
-            if (dyn) {
+            if constexpr (dyn) {
                 if (next_bid(r) < 0) break;
             } else {
                 batch_of(j, t, b);
@@ -349,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int r = 0;
         for (int j = 0; dyn || j < total; ++j, ++r) {
             int t, b;
-            if (dyn) {
+            if constexpr (dyn) {
                 if (next_bid(r) < 0) break;
             } else {
                 batch_of(j, t, b);
@@ -394,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         for (int j = 0; dyn || j < total; ++j) {
             int t = 0, b, X0, Y0, Z0;
-            if (dyn) {
+            if constexpr (dyn) {
                 b = next_bid(r);
                 if (b < 0) break;
             } else {
@@ -415,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int i = 0; i < CW; ++i) v[c][i] = 0u;
             } else {
-                if (multi && etid == 0) {
+                if (multi && etid == 0) {  // (multi is constexpr: folded away otherwise)
                     const unsigned long long t0 = global_ns();
                     while (!mbar_try_wait(&d_full[s], ph)) {
                         if (published < committed && global_ns() - t0 > 2000ull) {
