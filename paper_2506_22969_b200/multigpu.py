@@ -352,14 +352,25 @@ class SlabStencil:
         return out
 
     def close(self):
+        """Release the plan (P2P halos: collective over the slab's ranks)."""
         import ctypes as C
 
         from ._capi import lib
 
         if self._peers_open or self._flags:
             import torch
+            import torch.distributed as dist
 
+            from ._capi import check
+
+            # P2P: neighbours store into this rank's buffers until their last step;
+            # wait for them (stream flags), then for every rank (collective close)
+            if self.halo == "p2p" and getattr(self, "_peer_flag", None):
+                for which in self._peer_flag:
+                    check(lib().sst_stream_wait_geq_u32(None, C.c_void_p(self._flags + 4 * which), self._launch))
             torch.cuda.synchronize(torch.device("cuda", self.device))
+            if self.halo == "p2p" and dist.is_initialized():
+                dist.barrier(group=self.group)
         for p in self._peers_open:
             lib().sst_ipc_close(C.c_void_p(p))
         self._peers_open = []

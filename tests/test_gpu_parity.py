@@ -275,7 +275,8 @@ def test_multistep_launch_equals_single_steps(gpu, monkeypatch, name, dims, step
 
 # ---- split-operand precision (SST_PREC_F16X2): B'' = B_hi + B_lo, ~fp32 steps
 @pytest.mark.parametrize("name,dims", [("Box-2D9P", (300, 517)), ("Star-2D13P", (130, 129)),
-                                       ("Box-3D27P", (33, 17, 129)), ("Heat-3D", (20, 24, 40))])
+                                       ("Box-3D27P", (33, 17, 129)), ("Heat-3D", (20, 24, 40)),
+                                       ("1D5P", (100003,))])
 def test_f16x2_one_step_bit_exact(gpu, name, dims):
     g = oracle.random_grid(dims, seed=4)
     eng = SparseStencil(name, list(dims), precision="f16x2")
