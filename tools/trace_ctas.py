@@ -1,6 +1,6 @@
 """Per-CTA timeline of one launch (profiling aid, not a bench): SM id, prologue,
 main-loop and end timestamps from %globaltimer, summarised as spread statistics.
-Usage: python tools/trace_ctas.py Box-3D27P 512x512x512 [variant] [launches=5]
+Usage: [FLUSH=1] python tools/trace_ctas.py Box-3D27P 512x512x512 [variant] [launches=5]
 """
 import os
 import sys
@@ -28,7 +28,12 @@ buf = torch.zeros(4 * ctas, dtype=torch.int64, device="cuda")
 eng.run(3)
 torch.cuda.synchronize()
 check(lib().sst_plan_set_trace(eng._h, C.c_void_p(buf.data_ptr())))
+flush = torch.empty(64 << 20, dtype=torch.int32, device="cuda") if os.environ.get("FLUSH") else None
 for i in range(launches):
+    if flush is not None:  # bench.py's L2 flush: write then read 256 MB
+        flush.fill_(i)
+        flush.sum()
+        torch.cuda.synchronize()
     eng.run(steps, src=(i * steps) & 1)
     torch.cuda.synchronize()
     t = buf.view(ctas, 4).cpu()
