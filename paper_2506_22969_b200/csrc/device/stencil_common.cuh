@@ -60,7 +60,8 @@ struct StepParams {
     int32_t patch_w, patch_h, patch_planes;
     int32_t debug_mode;        // ablation bits (profiling only): 1 no stores, 2 no gather, 4 no MMA,
                                // 8 no right-edge plain stores, 16 TMA loads only (3D),
-                               // 32 stores only (zeros), 16 TMA loads only (3D stream kernel)
+                               // 32 stores only (zeros), 64 staging without TMA stores,
+                               // 128 TMA stores without staging
     int32_t tmem_cols;         // TMEM allocation (power of two >= the kernel's column budget)
     int32_t zchunk;            // 3D stream kernel: output planes per (band, z-chunk) run; 0 = whole column
     int32_t lo_sweep0;         // first gather sweep writing B_lo rows (SST_PREC_F16X2); = k_pad/32 otherwise
@@ -391,6 +392,7 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
     for (int c = 0; c < NBOX; ++c)
 #pragma unroll
         for (int i = 0; i < CW; ++i) {
+            if (p.debug_mode & 128) break;  // ablation: no staging stores
             // local output (x, y) of D row m = 32q + lane in tile (2c + (i&1), i/2); the
             // 16-byte chunk index is XOR-swizzled with (row % 8) as TMA SWIZZLE_128B expects
             const uint32_t y = static_cast<uint32_t>(i / 2) * kTileH + dy;
@@ -407,7 +409,7 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
     if constexpr (DIMS == 2)
         if (p.peer_mask != 0 && etid >= 32 && etid < 64 && (Y0 < p.r || Y0 + TYB * kTileH > p.peer_down0))
             peer_right_edge(p, stage, s_stride, X0, Y0, TYB * kTileH, peer_up_buf, peer_down_buf, lane);
-    if (etid == 0) {
+    if (etid == 0 && !(p.debug_mode & 64)) {  // (ablation 64: staging only, no TMA stores)
         fence_proxy_async_smem();
 #pragma unroll
         for (int c = 0; c < NBOX; ++c) {
