@@ -105,7 +105,7 @@ struct Variant {
                    bool cooperative);
 };
 
-template <int D, int TYB, int NP, bool AT>
+template <int D, int TYB, int NP, bool AT, int NS = sst::kStageBufs>
 Variant make_variant() {
     Variant v{};
     v.dims = D;
@@ -114,18 +114,21 @@ Variant make_variant() {
     v.a_tmem = AT;
     v.acc_cols = 2 * sst::kTXB * TYB;
     v.layout = [](int nks, int k_pad, int pw, int ph, int planes) {
-        return sst::smem_layout<TYB, NP, AT>(nks, k_pad, pw, ph, planes);
+        return sst::smem_layout<TYB, NP, AT, NS>(nks, k_pad, pw, ph, planes);
     };
     // 2D: one instantiation per time-loop mode (static / dynamic / multi-step)
     v.configure = [](int smem) {
-        ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeStatic>,
+        ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeStatic, NS>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
            "cudaFuncSetAttribute");
         if constexpr (D == 2) {
-            ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeDynamic>,
+            ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeDynamic, NS>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                "cudaFuncSetAttribute");
-            ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMulti>,
+            ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMulti, NS>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+               "cudaFuncSetAttribute");
+            ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModePeer, NS>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                "cudaFuncSetAttribute");
         }
@@ -135,13 +138,16 @@ Variant make_variant() {
                   bool coop) {
         if constexpr (D == 2) {
             if (p.nsteps > 1)
-                return launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMulti>, grid, smem, st, maps,
-                                  p, coop);
+                return launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMulti, NS>, grid, smem, st,
+                                  maps, p, coop);
+            if (p.sched && p.peer_mask)
+                return launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModePeer, NS>, grid, smem, st,
+                                  maps, p, coop);
             if (p.sched)
-                return launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeDynamic>, grid, smem, st,
+                return launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeDynamic, NS>, grid, smem, st,
                                   maps, p, coop);
         }
-        launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeStatic>, grid, smem, st, maps, p, coop);
+        launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeStatic, NS>, grid, smem, st, maps, p, coop);
     };
     return v;
 }
@@ -195,6 +201,9 @@ const Variant* variants(int& n) {
         make_stream_variant<8, 2, 3, true, 2, 5, 2>(), make_stream_variant<8, 2, 3, true, 2, 4, 2>(),
         // 3D whole-window kernel (kz != 3 or non-streamable layouts): 25-27
         make_variant<3, 2, 4, false>(), make_variant<3, 2, 3, false>(), make_variant<3, 2, 2, false>(),
+        // 2D with two output staging buffers (28-31): <D, TYB, NP, AT, NS>
+        make_variant<2, 4, 4, true, 2>(), make_variant<2, 8, 2, true, 2>(), make_variant<2, 4, 3, true, 2>(),
+        make_variant<2, 8, 3, true, 2>(),
     };
     n = static_cast<int>(sizeof(v) / sizeof(v[0]));
     return v;
@@ -511,8 +520,9 @@ struct sst_plan {
             const char* dyn_e = std::getenv("SST_DYN");
             // (few batches per CTA: static striding measured faster, e.g. Heat-2D 4096^2
             // L2-cold 28.6 vs 29.9 us; SST_DYN=1 forces dynamic, 0 static)
+            // (2D P2P halos: only the dynamic-peer instantiation carries the peer stores)
             const bool dyn = !multi && variant->multistep &&
-                             (dyn_e ? std::atoi(dyn_e) != 0 : p.nbatch >= 24 * grid);
+                             (p.peer_mask != 0 || (dyn_e ? std::atoi(dyn_e) != 0 : p.nbatch >= 24 * grid));
             if (dyn && !d_sched) {
                 ck(cudaMalloc(&d_sched, 4), "cudaMalloc(sched)");
                 ck(cudaMemsetAsync(d_sched, 0, 4, st), "cudaMemsetAsync(sched)");

@@ -351,7 +351,7 @@ __device__ __forceinline__ void peer_right_edge(const StepParams& p, uint32_t st
 //               (and leave partially written 32-byte sectors behind).
 enum EdgeMode { kEdgePlain = 0, kEdgeRing = 1 };
 
-template <int DIMS, int TYB, int NS, int EDGE = kEdgePlain>
+template <int DIMS, int TYB, int NS, int EDGE = kEdgePlain, bool PEER = true>
 __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorMap* tmap_out, float* dst,
                                             uint32_t (&v)[kTXB / 2][2 * TYB], uint8_t* sS,
                                             uint32_t s_stride, int nb, int X0, int Y0, int Z0,
@@ -388,11 +388,11 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
     const uint32_t stage = smem_u32(sS) + buf;
     if (etid == 0) bulk_wait_read<NS - 1>();  // this buffer's previous stores have read it
     named_bar_sync(kEpiBarrier, kEpiWarps * 32);
+    if (!(p.debug_mode & 128)) {  // (ablation 128: TMA stores without staging)
 #pragma unroll
     for (int c = 0; c < NBOX; ++c)
 #pragma unroll
         for (int i = 0; i < CW; ++i) {
-            if (p.debug_mode & 128) break;  // ablation: no staging stores
             // local output (x, y) of D row m = 32q + lane in tile (2c + (i&1), i/2); the
             // 16-byte chunk index is XOR-swizzled with (row % 8) as TMA SWIZZLE_128B expects
             const uint32_t y = static_cast<uint32_t>(i / 2) * kTileH + dy;
@@ -401,12 +401,13 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
                          "r"(v[c][i])
                          : "memory");
         }
+    }
     // The named barrier drains every epilogue thread's staging stores (bar.sync has
     // CTA memory-ordering semantics); the issuing thread then orders them before its
     // async-proxy (TMA) reads with one proxy fence. A per-thread fence right after the
     // stores instead costs each thread a MEMBAR over its 32-64 stores in flight.
     named_bar_sync(kEpiBarrier, kEpiWarps * 32);
-    if constexpr (DIMS == 2)
+    if constexpr (DIMS == 2 && PEER)
         if (p.peer_mask != 0 && etid >= 32 && etid < 64 && (Y0 < p.r || Y0 + TYB * kTileH > p.peer_down0))
             peer_right_edge(p, stage, s_stride, X0, Y0, TYB * kTileH, peer_up_buf, peer_down_buf, lane);
     if (etid == 0 && !(p.debug_mode & 64)) {  // (ablation 64: staging only, no TMA stores)
@@ -424,7 +425,7 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
         // into the neighbours' halo slices (NVLink stores of the same staged boxes;
         // the peer maps span only the r halo slices, TMA clips everything else)
         const int slice0 = DIMS == 2 ? Y0 : Z0, nslice = DIMS == 2 ? TYB * kTileH : 1;
-        if (peer_up != nullptr && slice0 < p.r) {
+        if (PEER && peer_up != nullptr && slice0 < p.r) {
 #pragma unroll 1
             for (int c = 0; c < NBOX; ++c) {
                 const int bx0 = X0 + c * kBoxW;
@@ -435,7 +436,7 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
                     tma_store_3d(peer_up, sS + buf + c * s_stride, bx0, Y0, Z0);
             }
         }
-        if (peer_down != nullptr && slice0 + nslice > p.peer_down0) {
+        if (PEER && peer_down != nullptr && slice0 + nslice > p.peer_down0) {
 #pragma unroll 1
             for (int c = 0; c < NBOX; ++c) {
                 const int bx0 = X0 + c * kBoxW;

@@ -71,12 +71,12 @@ __host__ __device__ inline SmemLayout smem_layout_generic(int nks, int k_pad, in
 // rings, 3 + 2 + 2 deep).
 constexpr int kBidSlots = 16;
 
-template <int TYB, int NP, bool AT>
+template <int TYB, int NP, bool AT, int NS = kStageBufs>
 __host__ __device__ inline SmemLayout smem_layout(int nks, int k_pad, int patch_w, int patch_h,
                                                   int planes) {
     static_assert(kBidSlots > NP + 4, "batch-index ring vs pipeline depth");
     SmemLayout L = smem_layout_generic<TYB>(nks, k_pad, patch_w, patch_h, planes, NP, 2, 2 * NP + 8 + kBidSlots,
-                                            kStageBufs, AT);
+                                            NS, AT);
     L.ring = align_up(L.total, 16);  // the batch-index ring (int32 x kBidSlots)
     L.total = align_up(L.ring + kBidSlots * 4, 128);
     return L;
@@ -122,9 +122,13 @@ __device__ __forceinline__ uint32_t refresh_min(const StepParams& p, uint32_t ne
 // MODE (compile-time, so each launch runs only its own code path: the kernel's
 // instruction footprint matters for L2-cold launches): 0 static batch striding,
 // 1 dynamic batches (p.sched), 2 multi-step dataflow (p.nsteps > 1, p.flags).
-enum StepMode { kModeStatic = 0, kModeDynamic = 1, kModeMulti = 2 };
+// 3 = dynamic batches with the slab P2P halo stores (the only 2D instantiation that
+// carries the peer code: it measurably slowed the store path of the others).
+enum StepMode { kModeStatic = 0, kModeDynamic = 1, kModeMulti = 2, kModePeer = 3 };
 
-template <int DIMS, int TYB, int NP, bool AT, int MODE = kModeStatic>
+// NS: output staging buffers (TMA stores of batch n read one while batch n + 1 stages
+// into the next; 1 = the epilogue waits for each batch's stores to leave smem)
+template <int DIMS, int TYB, int NP, bool AT, int MODE = kModeStatic, int NS = kStageBufs>
 __global__ void __launch_bounds__(kThreads, 1)
     stencil_step_kernel(const __grid_constant__ MapSet maps, const StepParams p) {
     constexpr int N = kTXB * TYB;
@@ -138,7 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     using namespace ptx;
 
     extern __shared__ __align__(1024) uint8_t smem[];
-    const SmemLayout L = smem_layout<TYB, NP, AT>(p.nks, p.k_pad, p.patch_w, p.patch_h, p.patch_planes);
+    const SmemLayout L = smem_layout<TYB, NP, AT, NS>(p.nks, p.k_pad, p.patch_w, p.patch_h, p.patch_planes);
     uint8_t* sA = smem + L.a;
     uint8_t* sB = smem + L.b;  // 2 stages
     uint8_t* sS = smem + L.s;  // output staging
@@ -224,7 +228,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     constexpr bool multi = MODE == kModeMulti;
     // single-step launches with a scheduler counter draw batches dynamically
-    constexpr bool dyn = MODE == kModeDynamic;
+    constexpr bool dyn = MODE == kModeDynamic || MODE == kModePeer;
+    constexpr bool peer = MODE == kModePeer || DIMS == 3;  // (3D whole-window: one instantiation)
     auto next_bid = [&](int r) {  // consumers: batch index of real iteration r (-1: done)
         mbar_wait(&bid_full[r % kBidSlots], (r / kBidSlots) & 1);
         return sBid[r % kBidSlots];
@@ -440,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (!(p.debug_mode & 1))
             {
                 const int par = (p.src + t + 1) & 1;
-                store_batch<DIMS, TYB, kStageBufs>(
+                store_batch<DIMS, TYB, NS, kEdgePlain, peer>(
                     p, &maps.out[par], buf_of(p, par), v, sS, L.s_stride, r - 1, X0, Y0, Z0, q, lane, etid,
                     nullptr, (p.peer_mask & 1) ? &p.peer_maps->up[par] : nullptr,
                     (p.peer_mask & 2) ? &p.peer_maps->down[par] : nullptr, par ? p.peer_up_buf[1] : p.peer_up_buf[0],
