@@ -165,14 +165,20 @@ Variant make_stream_variant() {
         return sst::smem_layout_stream<TYB, NP, KZ, NB, NACC, NS, AT>(nks, k_pad, pw, ph);
     };
     v.configure = [](int smem) {
-        ck(cudaFuncSetAttribute(sst::stencil3d_stream_kernel<TYB, NP, KZ, NB, NACC, NS, AT>,
+        ck(cudaFuncSetAttribute(sst::stencil3d_stream_kernel<TYB, NP, KZ, NB, NACC, NS, AT, false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+           "cudaFuncSetAttribute");
+        ck(cudaFuncSetAttribute(sst::stencil3d_stream_kernel<TYB, NP, KZ, NB, NACC, NS, AT, true>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
            "cudaFuncSetAttribute");
     };
     v.multistep = false;
     v.launch = [](int grid, int smem, cudaStream_t st, const sst::MapSet& maps, const sst::StepParams& p,
                   bool coop) {
-        launch_pdl(sst::stencil3d_stream_kernel<TYB, NP, KZ, NB, NACC, NS, AT>, grid, smem, st, maps, p, coop);
+        if (p.peer_mask)
+            return launch_pdl(sst::stencil3d_stream_kernel<TYB, NP, KZ, NB, NACC, NS, AT, true>, grid, smem, st, maps,
+                              p, coop);
+        launch_pdl(sst::stencil3d_stream_kernel<TYB, NP, KZ, NB, NACC, NS, AT, false>, grid, smem, st, maps, p, coop);
     };
     return v;
 }

@@ -64,7 +64,8 @@ __device__ __forceinline__ void for_each_run(int u0, int u1, int ozw, int nby, i
 // NB: B'' ring depth, NACC (> KZ): accumulator ring, NS: output staging buffers,
 // AT: compressed A'' in TMEM instead of smem (frees smem and its bandwidth: with
 // N = 32 the per-MMA A reads were the largest smem stream of the 3D kernel).
-template <int TYB, int NP, int KZ, int NB, int NACC, int NS, bool AT>
+// PEER: the slab P2P halo stores are compiled in (launched only when p.peer_mask != 0)
+template <int TYB, int NP, int KZ, int NB, int NACC, int NS, bool AT, bool PEER = false>
 __global__ void __launch_bounds__(kThreads, 1)
     stencil3d_stream_kernel(const __grid_constant__ MapSet maps, const StepParams p) {
     constexpr int N = kTXB * TYB;
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ring = sRing + (ci % kRingSlots) * (TYB * kTileH * 4);
                 }
                 if (!(p.debug_mode & 1))
-                    store_batch<3, TYB, NS, kEdgeRing>(
+                    store_batch<3, TYB, NS, kEdgeRing, PEER>(
                         p, tmap_out, buf_of(p, p.src ^ 1), v, sS, L.s_stride, o, X0, Y0, p.slow_lo + zo, q, lane,
                         etid, ring, (p.peer_mask & 1) ? &p.peer_maps->up[p.src ^ 1] : nullptr,
                         (p.peer_mask & 2) ? &p.peer_maps->down[p.src ^ 1] : nullptr);
