@@ -23,15 +23,22 @@
 namespace sst {
 
 // Right-edge ring cache (see kEdgeRing in stencil_common.cuh): one slot per
-// gathered input plane, kRingSlots deep. Slot reuse is safe by pipeline depth: the
-// gather of plane it + kRingSlots waits (b_empty) for the MMA of plane
-// it + kRingSlots - NB, which waited (d_empty) for the epilogue to drain output
-// it + kRingSlots - NB - NACC - R > it - R, the last reader of slot it.
-constexpr int kRingSlots = 16;
+// gathered input plane, ring_slots<NP, NB, NACC>() deep. The PRODUCER fills slot
+// it % slots when it issues plane it; slot reuse is safe by pipeline depth: the
+// producer issues plane it + slots only after the gather of plane it + slots - NP
+// (patch_empty), which waited (b_empty) for the MMA of plane it + slots - NP - NB,
+// which waited (d_empty) for the epilogue to release output it + slots - NP - NB -
+// NACC; with slots > NP + NB + NACC that is past output it - R + 1, so the last
+// reader of slot it (output it - R, center plane it) is done.
+template <int NP, int NB, int NACC>
+__host__ __device__ constexpr int ring_slots() {
+    return NP + NB + NACC + 1 <= 16 ? 16 : 32;
+}
 
 template <int TYB, int NP, int KZ, int NB, int NACC, int NS, bool AT>
 __host__ __device__ inline SmemLayout smem_layout_stream(int nks, int k_pad, int patch_w, int patch_h) {
-    static_assert(kRingSlots > NB + NACC + (KZ - 1) / 2, "ring cache slots vs pipeline depth");
+    constexpr int kRingSlots = ring_slots<NP, NB, NACC>();
+    static_assert(kRingSlots > NP + NB + NACC, "ring cache slots vs pipeline depth");
     SmemLayout L = smem_layout_generic<TYB>(nks, k_pad, patch_w, patch_h, 1, NP, NB,
                                             2 * NP + 2 * NB + 2 * NACC + kRingSlots, NS, AT);
     L.ring = align_up(L.total, 16);
@@ -74,6 +81,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int NGROUP = N / 8;
     constexpr int GPW = NGROUP >= kGatherWarps ? NGROUP / kGatherWarps : 1;
     constexpr int R = (KZ - 1) / 2;
+    constexpr int kRingSlots = ring_slots<NP, NB, NACC>();
     static_assert(NACC > KZ, "one accumulator beyond the KZ open ones");
     static_assert(N % 16 == 0 && N <= 128, "UMMA N for M=128");
     static_assert(NACC * N <= 320, "accumulator ring must leave TMEM room for metadata / A''");

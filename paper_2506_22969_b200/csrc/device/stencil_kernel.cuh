@@ -25,7 +25,7 @@ namespace sst {
 struct SmemLayout {
     uint32_t a, b, b_stride, p, p_stride, s, s_stride, gsrc, gdst, bars, tmem_slot, total;
     uint32_t pbar;  // prologue mbarrier (constant staging by bulk copy)
-    uint32_t ring;  // 3D stream kernel: right-edge ring-value cache (kRingSlots x TYB*8 x 4 floats)
+    uint32_t ring;  // 3D stream kernel: right-edge ring-value cache (ring_slots() x TYB*8 x 4 floats)
 };
 
 __host__ __device__ inline uint32_t align_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
