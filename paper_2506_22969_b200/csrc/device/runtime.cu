@@ -527,7 +527,8 @@ struct sst_plan {
             // (few batches per CTA: static striding measured faster, e.g. Heat-2D 4096^2
             // L2-cold 28.6 vs 29.9 us; SST_DYN=1 forces dynamic, 0 static)
             // (2D P2P halos: only the dynamic-peer instantiation carries the peer stores)
-            const bool dyn = !multi && variant->multistep &&
+            // (the store-only ablation, debug bit 32, has no producer to draw batches)
+            const bool dyn = !multi && variant->multistep && !(debug_mode & 32) &&
                              (p.peer_mask != 0 || (dyn_e ? std::atoi(dyn_e) != 0 : p.nbatch >= 24 * grid));
             if (dyn && !d_sched) {
                 ck(cudaMalloc(&d_sched, 4), "cudaMalloc(sched)");
