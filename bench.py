@@ -407,6 +407,8 @@ def main():
     if args.steps is None:
         args.steps = cfg[2]
     args.warmup = max(3, args.warmup)
+    if args.fuse < 1 or args.steps % args.fuse:
+        ap.error(f"--steps ({args.steps}) must be a positive multiple of --fuse ({args.fuse})")
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -210,6 +210,10 @@ const Variant* variants(int& n) {
         // 2D with two output staging buffers (28-31): <D, TYB, NP, AT, NS>
         make_variant<2, 4, 4, true, 2>(), make_variant<2, 8, 2, true, 2>(), make_variant<2, 4, 3, true, 2>(),
         make_variant<2, 8, 3, true, 2>(),
+        // 3D z-streaming with KZ = 5 (temporally fused 3D stencils, k = 5: 40 K steps of A''):
+        // 32-35 <TYB, NP, KZ, AT>
+        make_stream_variant<2, 4, 5, true>(), make_stream_variant<2, 6, 5, true>(),
+        make_stream_variant<4, 3, 5, false>(), make_stream_variant<2, 4, 5, false>(),
     };
     n = static_cast<int>(sizeof(v) / sizeof(v[0]));
     return v;

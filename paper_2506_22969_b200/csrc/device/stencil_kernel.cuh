@@ -50,6 +50,10 @@ __host__ __device__ inline SmemLayout smem_layout_generic(int nks, int k_pad, in
     L.p_stride = align_up(static_cast<uint32_t>(patch_w * patch_h * planes) * 4u, 128);
     L.p = o = align_up(o, 128);
     o += np * L.p_stride;
+    // the prologue stages the A'' image / metadata words in [L.b, L.gsrc) before
+    // moving them into TMEM: deep A'' (fused 3D, 40 K steps) needs more than the rings
+    const uint32_t scratch = prologue_scratch_bytes(nks, a_in_tmem);
+    if (o < L.b + scratch) o = L.b + scratch;
     L.gsrc = o = align_up(o, 16);
     o += static_cast<uint32_t>(k_pad) * 4u;
     L.gdst = o;

@@ -190,12 +190,14 @@ def test_full_size_multi_step_windows(gpu):
         assert np.abs(got - want).max() <= tol_abs(steps)
 
 
-@pytest.mark.parametrize("name,fuse", [("Box-2D9P", 2), ("Heat-2D", 3), ("Box-2D9P", 4)])
+@pytest.mark.parametrize("name,fuse", [("Box-2D9P", 2), ("Heat-2D", 3), ("Box-2D9P", 4), ("Box-3D27P", 2),
+                                       ("Heat-3D", 2)])
 def test_temporal_fusion(gpu, name, fuse):
     """fuse_time_steps (stencil.cpp:272-347) on the device: the fused operator's
     dyadic weights are exact in f16, so one fused launch on dyadic data equals
-    `fuse` reference steps exactly; longer runs stay within the f16 tolerance."""
-    dims = (140, 300)
+    `fuse` reference steps exactly; longer runs stay within the f16 tolerance.
+    3D: the fused k = 5 operator runs on the KZ = 5 z-streaming kernels."""
+    dims = (26, 40, 150) if "3D" in name else (140, 300)
     g = oracle.random_grid(dims, 12)
     eng = SparseStencil(name, list(dims), fuse=fuse)
     one = valid_core(eng.apply_host(g.astype(np.float32), fuse), fuse, eng.r).astype(np.float64)
