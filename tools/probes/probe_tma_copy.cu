@@ -54,6 +54,46 @@ __global__ void __launch_bounds__(32, 1) box_copy(const __grid_constant__ CUtens
     sst::ptx::bulk_wait<0>();
 }
 
+// box loads by TMA (warp 0, as above) + the 128 x 64 output of each batch written with
+// coalesced 16-byte LSU stores by 4 warps (a warp writes 512 contiguous bytes per row);
+// cs: st.global.cs (streaming) instead of st.global
+template <bool CS>
+__global__ void __launch_bounds__(160, 1) box_lsu(const __grid_constant__ CUtensorMap tin, float* out, int np,
+                                                  int loads) {
+    extern __shared__ __align__(1024) uint8_t raw[];
+    Smem& S = *reinterpret_cast<Smem*>(raw + ((1024u - (sst::ptx::smem_u32(raw) & 1023u)) & 1023u));
+    const int nb = kNbx * kNby;
+    if (threadIdx.x < 32) {
+        if (threadIdx.x != 0 || !loads) return;
+        for (int s = 0; s < np; ++s) sst::ptx::mbar_init(&S.full[s], 1);
+        sst::ptx::fence_mbar_init();
+        int it = 0;
+        for (int b = blockIdx.x; b < nb; b += gridDim.x, ++it) {
+            const int X0 = (b % kNbx) * kBW, Y0 = (b / kNbx) * kBH;
+            const int s = it % np;
+            if (it >= np) sst::ptx::mbar_wait(&S.full[s], ((it / np) - 1) & 1);
+            sst::ptx::mbar_arrive_expect_tx(&S.full[s], kPW * kPH * 4);
+            sst::ptx::tma_load_2d(S.patch[s], &tin, &S.full[s], X0 > 4 ? X0 - 4 : 0, Y0);
+        }
+        for (int j = (it > np ? it - np : 0); j < it; ++j) sst::ptx::mbar_wait(&S.full[j % np], (j / np) & 1);
+        return;
+    }
+    const int t = threadIdx.x - 32, w = t / 32, lane = t % 32;
+    const float4* src = reinterpret_cast<const float4*>(S.out[0]);
+    for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+        const int X0 = (b % kNbx) * kBW, Y0 = (b / kNbx) * kBH + 1;
+        for (int row = w; row < kBH; row += 4) {
+            const float4 v = src[(row * 32 + lane) & 2047];
+            float4* dst = reinterpret_cast<float4*>(out + static_cast<size_t>(Y0 + row) * kN + X0) + lane;
+            if (CS)
+                asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(v.x), "f"(v.y), "f"(v.z),
+                             "f"(v.w) : "memory");
+            else
+                *dst = v;
+        }
+    }
+}
+
 // contiguous: each CTA copies 32 KB chunks (same total bytes as one batch's load + store)
 __global__ void __launch_bounds__(32, 1) linear_copy(const float* in, float* out, size_t chunks, int np) {
     extern __shared__ __align__(1024) uint8_t raw[];
@@ -125,6 +165,28 @@ int main(int argc, char** argv) {
         const double bytes = nbatch * ((mode != 2 ? kPW * kPH * 4.0 : 0) + (mode != 1 ? kBW * kBH * 4.0 : 0));
         printf("%-28s np %d: %8.1f us  moved %7.1f GB/s  algorithmic(8 B/cell) %7.1f GB/s\n", names[mode], np,
                best * 1e3, bytes / (best * 1e-3) / 1e9, mode == 0 ? alg / (best * 1e-3) / 1e9 : 0.0);
+    }
+    cudaFuncSetAttribute(box_lsu<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(box_lsu<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int variant = 0; variant < 4; ++variant) {
+        const bool cs = variant & 1, loads = variant < 2;
+        float bst = 1e30f;
+        for (int rep = 0; rep < 5; ++rep) {
+            cudaEventRecord(e0);
+            if (cs)
+                box_lsu<true><<<sms, 160, smem>>>(tin, b, np, loads);
+            else
+                box_lsu<false><<<sms, 160, smem>>>(tin, b, np, loads);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            bst = std::min(bst, ms);
+        }
+        const double bytes = nbatch * ((loads ? kPW * kPH * 4.0 : 0) + kBW * kBH * 4.0);
+        printf("%-28s np %d: %8.1f us  moved %7.1f GB/s  algorithmic(8 B/cell) %7.1f GB/s\n",
+               loads ? (cs ? "TMA loads + LSU st.cs" : "TMA loads + LSU st") : (cs ? "LSU st.cs only" : "LSU st only"),
+               np, bst * 1e3, bytes / (bst * 1e-3) / 1e9, loads ? alg / (bst * 1e-3) / 1e9 : 0.0);
     }
     float best = 1e30f;
     const size_t chunks = cells * 4 / 32768;
