@@ -15,3 +15,9 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:sten
   -o $out/prof_box2d python bench.py --steps 4 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:stencil3d -s 3 -c 1 \
   -o $out/prof_box3d python bench.py --config box3d --steps 4 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:stencil_step -s 3 -c 1 \
+  -o $out/prof_star2d python bench.py --config star2d --steps 4 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:stencil_step -s 8 -c 1 \
+  -o $out/prof_heat2d python bench.py --config heat2d --steps 10 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
+# summaries (run here afterwards): for k in box2d box3d star2d heat2d; do
+#   python tools/ncu_summary.py $out/prof_$k.ncu-rep > profiles/<round>/ncu_${k}_full.txt; done
