@@ -528,12 +528,13 @@ struct sst_plan {
             // single-step 2D launches draw batches from a counter (load balance: the
             // static stride leaves a 15-20 % spread of CTA finish times); SST_DYN=0 off
             const char* dyn_e = std::getenv("SST_DYN");
-            // (few batches per CTA: static striding measured faster, e.g. Heat-2D 4096^2
-            // L2-cold 28.6 vs 29.9 us; SST_DYN=1 forces dynamic, 0 static)
+            // (few batches per CTA: static striding; Heat-2D 4096^2, 14 batches per CTA,
+            // back to back: dynamic 25.3-25.4 vs static 25.6-26.0 us; SST_DYN=1 forces
+            // dynamic, 0 static)
             // (2D P2P halos: only the dynamic-peer instantiation carries the peer stores)
             // (the store-only ablation, debug bit 32, has no producer to draw batches)
             const bool dyn = !multi && variant->multistep && !(debug_mode & 32) &&
-                             (p.peer_mask != 0 || (dyn_e ? std::atoi(dyn_e) != 0 : p.nbatch >= 24 * grid));
+                             (p.peer_mask != 0 || (dyn_e ? std::atoi(dyn_e) != 0 : p.nbatch >= 8 * grid));
             if (dyn && !d_sched) {
                 ck(cudaMalloc(&d_sched, 4), "cudaMalloc(sched)");
                 ck(cudaMemsetAsync(d_sched, 0, 4, st), "cudaMemsetAsync(sched)");
