@@ -188,13 +188,14 @@ Variant make_stream_variant() {
 // experiments; SST_A_SMEM=1 skips the A''-in-TMEM variants)
 const Variant* variants(int& n) {
     static const Variant v[] = {
-        // 2D (measured order, tools/ablate.py): 0 TMEM-A 8x3 (Box-2D9P 8192^2 multi-step
-        // 85.7 us = smem-A; Heat-2D 4096^2 single L2-cold launch 28.9 vs 30.7 us), 1 TMEM-A
-        // 4x4 (Star-2D13P 16384^2: 417 us vs 433 for smem-A 4x4), 2 smem-A 8x3, then the rest
-        make_variant<2, 8, 3, true>(), make_variant<2, 4, 4, true>(), make_variant<2, 8, 3, false>(),
-        make_variant<2, 4, 4, false>(), make_variant<2, 4, 2, true>(), make_variant<2, 8, 2, false>(),
-        make_variant<2, 4, 2, false>(), make_variant<2, 8, 4, false>(), make_variant<2, 8, 4, true>(),
-        make_variant<2, 8, 2, true>(),
+        // 2D (measured order, tools/ablate.py, after the P2P stores moved to their own
+        // instantiation): 0 TMEM-A 8x3 with two staging buffers (Box-2D9P 8192^2 83.4 us,
+        // Heat-2D 4096^2 25.0 vs 25.4 us for one buffer), 1 TMEM-A 8x2 (Star-2D13P
+        // 16384^2: 355 us vs 376 for TMEM-A 4x4), 2 TMEM-A 8x3, 3 TMEM-A 4x4, then smem-A
+        make_variant<2, 8, 3, true, 2>(), make_variant<2, 8, 2, true>(), make_variant<2, 8, 3, true>(),
+        make_variant<2, 4, 4, true>(), make_variant<2, 8, 3, false>(), make_variant<2, 4, 4, false>(),
+        make_variant<2, 4, 2, true>(), make_variant<2, 8, 2, false>(), make_variant<2, 4, 2, false>(),
+        make_variant<2, 8, 4, false>(),
         // 3D z-streaming (10-16): TMEM-A TYB 4 NP 4 (Box-3D27P 512^3: 206 us vs 222 smem-A), ...
         make_stream_variant<4, 4, 3, true>(), make_stream_variant<4, 3, 3, true>(),
         make_stream_variant<8, 3, 3, true>(), make_stream_variant<4, 2, 3, true>(),
@@ -207,9 +208,9 @@ const Variant* variants(int& n) {
         make_stream_variant<8, 2, 3, true, 2, 5, 2>(), make_stream_variant<8, 2, 3, true, 2, 4, 2>(),
         // 3D whole-window kernel (kz != 3 or non-streamable layouts): 25-27
         make_variant<3, 2, 4, false>(), make_variant<3, 2, 3, false>(), make_variant<3, 2, 2, false>(),
-        // 2D with two output staging buffers (28-31): <D, TYB, NP, AT, NS>
-        make_variant<2, 4, 4, true, 2>(), make_variant<2, 8, 2, true, 2>(), make_variant<2, 4, 3, true, 2>(),
-        make_variant<2, 8, 3, true, 2>(),
+        // more 2D (28-31): <D, TYB, NP, AT, NS>
+        make_variant<2, 8, 4, true>(), make_variant<2, 4, 4, true, 2>(), make_variant<2, 8, 2, true, 2>(),
+        make_variant<2, 4, 3, true, 2>(),
         // 3D z-streaming with KZ = 5 (temporally fused 3D stencils, k = 5: 40 K steps of A''):
         // 32-35 <TYB, NP, KZ, AT>
         make_stream_variant<2, 4, 5, true>(), make_stream_variant<2, 6, 5, true>(),
