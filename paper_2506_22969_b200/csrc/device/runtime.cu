@@ -131,12 +131,18 @@ Variant make_variant() {
             ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModePeer, NS>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                "cudaFuncSetAttribute");
+            ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMultiDyn, NS>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+               "cudaFuncSetAttribute");
         }
     };
     v.multistep = D == 2;
     v.launch = [](int grid, int smem, cudaStream_t st, const sst::MapSet& maps, const sst::StepParams& p,
                   bool coop) {
         if constexpr (D == 2) {
+            if (p.multi_dyn)
+                return launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMultiDyn, NS>, grid, smem, st,
+                                  maps, p, coop);
             if (p.nsteps > 1)
                 return launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMulti, NS>, grid, smem, st,
                                   maps, p, coop);
@@ -252,7 +258,8 @@ struct sst_plan {
                               // out[i]: stores into buffer i, clipped to the interior (and row window)
     uint32_t* d_sched = nullptr;  // dynamic batch counter of single-step 2D launches
     uint32_t sched_base = 0;
-    uint32_t* d_flags = nullptr;  // per-batch step counters of multi-step launches
+    uint32_t* d_flags = nullptr;  // progress words of multi-step launches (per CTA / per batch)
+    int flag_mode = 0;            // what d_flags counts: 1 per-CTA iterations, 2 per-batch steps
     int flags_n = 0;
     uint32_t flag_base = 0;
     bool tmap_ok = false;
@@ -493,13 +500,16 @@ struct sst_plan {
         // multi-step dataflow launch, whose static batch ownership inherits the
         // 15-20 % spread of per-SM speed). SST_MULTISTEP=1 selects the multi-step
         // launch (read per call: tests toggle it).
+        // SST_MULTISTEP=2: the multi-step launch with dynamic batch ownership
         const char* ms_e = std::getenv("SST_MULTISTEP");
         const bool ms_env = ms_e && std::atoi(ms_e) != 0;
+        const bool ms_dyn = ms_e && std::atoi(ms_e) == 2;
         const bool full = !(y_hi > y_lo);
         // (a fold's view rows depend on the next row's first cells: outside the
         // multi-step kernel's 3 x 3 batch neighbourhood, so folds run per step)
         const bool multi = ms_env && variant->multistep && full && nsteps > 1 && !fold_n && !peer_buf[0][0] &&
                            !peer_buf[1][0];
+        const bool mdyn = multi && ms_dyn;
         if (multi && flags_n < p.nbatch) {
             cudaFree(d_flags);
             d_flags = nullptr;
@@ -507,6 +517,13 @@ struct sst_plan {
             ck(cudaMemsetAsync(d_flags, 0, static_cast<size_t>(p.nbatch) * 4, st), "cudaMemsetAsync(flags)");
             flags_n = p.nbatch;
             flag_base = 0;
+        }
+        // the two multi-step modes count different things in the flag words (per CTA /
+        // per batch): restart the counters when the mode changes
+        if (multi && flag_mode != (mdyn ? 2 : 1)) {
+            ck(cudaMemsetAsync(d_flags, 0, static_cast<size_t>(flags_n) * 4, st), "cudaMemsetAsync(flags)");
+            flag_base = 0;
+            flag_mode = mdyn ? 2 : 1;
         }
         int cur = src;
         uint64_t left = nsteps;
@@ -521,7 +538,9 @@ struct sst_plan {
         }
         while (left > 0) {
             // chunks keep flag counters far from wrap-around between resets
-            const uint64_t chunk = multi ? std::min<uint64_t>(left, 1u << 16) : 1;
+            // (mdyn: items t * nbatch + b stay below 2^31)
+            const uint64_t cap = mdyn ? std::max<uint64_t>(1, 0x7fffffffu / static_cast<uint64_t>(p.nbatch)) : 1u << 16;
+            const uint64_t chunk = multi ? std::min<uint64_t>({left, uint64_t{1} << 16, cap}) : 1;
             p = step_params(cur);
             p.nsteps = static_cast<int32_t>(chunk);
             p.flags = d_flags;
@@ -534,8 +553,8 @@ struct sst_plan {
             // dynamic, 0 static)
             // (2D P2P halos: only the dynamic-peer instantiation carries the peer stores)
             // (the store-only ablation, debug bit 32, has no producer to draw batches)
-            const bool dyn = !multi && variant->multistep && !(debug_mode & 32) &&
-                             (p.peer_mask != 0 || (dyn_e ? std::atoi(dyn_e) != 0 : p.nbatch >= 8 * grid));
+            const bool dyn = mdyn || (!multi && variant->multistep && !(debug_mode & 32) &&
+                                      (p.peer_mask != 0 || (dyn_e ? std::atoi(dyn_e) != 0 : p.nbatch >= 8 * grid)));
             if (dyn && !d_sched) {
                 ck(cudaMalloc(&d_sched, 4), "cudaMalloc(sched)");
                 ck(cudaMemsetAsync(d_sched, 0, 4, st), "cudaMemsetAsync(sched)");
@@ -543,11 +562,15 @@ struct sst_plan {
             }
             p.sched = dyn ? d_sched : nullptr;
             p.sched_base = sched_base;
-            variant->launch(grid, smem, st, maps, p, multi);
-            if (dyn) sched_base += static_cast<uint32_t>(p.nbatch);  // nbatch - grid draws + grid final ones
+            p.multi_dyn = mdyn ? 1 : 0;
+            variant->launch(grid, smem, st, maps, p, multi && !mdyn);
+            // (items - grid draws, plus one final draw per CTA)
+            if (dyn) sched_base += static_cast<uint32_t>(p.nbatch * (mdyn ? chunk : 1));
             ck(cudaGetLastError(), "kernel launch");
             ++launches;
-            if (multi) {  // per-CTA progress counters advance by nper iterations per step
+            if (mdyn) {  // per-batch step counters
+                flag_base += static_cast<uint32_t>(chunk);
+            } else if (multi) {  // per-CTA progress counters advance by nper iterations per step
                 const uint64_t nper = (static_cast<uint64_t>(p.nbatch) + grid - 1) / grid;
                 flag_base += static_cast<uint32_t>(nper * chunk);
             }

@@ -75,6 +75,7 @@ struct StepParams {
     float* peer_down_buf[2];
     uint32_t* sched;           // 2D single-step launches: global batch counter (dynamic scheduling), or null
     uint32_t sched_base;       // counter value at launch start
+    int32_t multi_dyn;         // 2D: the multi-step launch with dynamic batch ownership (kModeMultiDyn)
     unsigned long long* trace; // profiling only (sst_plan_set_trace): per CTA {smid, t_start, t_main, t_end}
 };
 

@@ -74,6 +74,10 @@ __host__ __device__ inline SmemLayout smem_layout_generic(int nks, int k_pad, in
 // kBidSlots iterations ahead of the epilogue through the patch / B'' / accumulator
 // rings, 3 + 2 + 2 deep).
 constexpr int kBidSlots = 16;
+// dynamic multi-step mode: items committed but not yet published (publication every
+// kPubEvery items, lagging kPubLag store groups)
+constexpr int kPubEvery = 8, kPubLag = 2, kPubRing = 16;
+static_assert(kPubRing >= kPubEvery + kPubLag + 1, "publication ring");
 
 template <int TYB, int NP, bool AT, int NS = kStageBufs>
 __host__ __device__ inline SmemLayout smem_layout(int nks, int k_pad, int patch_w, int patch_h,
@@ -81,8 +85,9 @@ __host__ __device__ inline SmemLayout smem_layout(int nks, int k_pad, int patch_
     static_assert(kBidSlots > NP + 4, "batch-index ring vs pipeline depth");
     SmemLayout L = smem_layout_generic<TYB>(nks, k_pad, patch_w, patch_h, planes, NP, 2, 2 * NP + 8 + kBidSlots,
                                             NS, AT);
-    L.ring = align_up(L.total, 16);  // the batch-index ring (int32 x kBidSlots)
-    L.total = align_up(L.ring + kBidSlots * 4, 128);
+    L.ring = align_up(L.total, 16);  // the batch-index ring (int32 x kBidSlots), then the
+                                     // dynamic multi-step mode's unpublished items (kPubRing)
+    L.total = align_up(L.ring + (kBidSlots + kPubRing) * 4, 128);
     return L;
 }
 
@@ -114,21 +119,26 @@ __device__ __forceinline__ uint32_t refresh_min(const StepParams& p, uint32_t ne
 
 // AT: compressed A'' in TMEM (tcgen05.mma.sp [a-tmem] form) instead of smem.
 //
-// One launch runs p.nsteps time steps (persistent CTAs; 2D, full window). Step t
-// reads buffer (src + t) & 1 and writes the other one. There is no grid-wide
-// barrier between steps: batch b's epilogue publishes flags[b] = flag_base + t + 1
-// once its step-t stores are complete, and the producer waits for the 3 x 3
-// neighbourhood's flags before loading b's patch for step t + 1. That ordering also
-// covers the write-after-read on the ping-pong buffer (a neighbour publishes only
-// after it loaded its step-t patch). CTAs walk batches in the same order every
-// step, so in steady state the flags are long set when checked: no per-step
-// launch, prologue or tail.
 // MODE (compile-time, so each launch runs only its own code path: the kernel's
-// instruction footprint matters for L2-cold launches): 0 static batch striding,
-// 1 dynamic batches (p.sched), 2 multi-step dataflow (p.nsteps > 1, p.flags).
-// 3 = dynamic batches with the slab P2P halo stores (the only 2D instantiation that
-// carries the peer code: it measurably slowed the store path of the others).
-enum StepMode { kModeStatic = 0, kModeDynamic = 1, kModeMulti = 2, kModePeer = 3 };
+// instruction footprint matters for L2-cold launches):
+//   0 static batch striding, one time step;
+//   1 dynamic batches (p.sched counter), one time step;
+//   2 multi-step dataflow with static batch ownership: one launch runs p.nsteps steps
+//     (persistent CTAs, 2D, full window), step t reads buffer (src + t) & 1; no grid
+//     barrier between steps: each CTA publishes a progress counter flags[cta] and a
+//     producer loads batch b of step t once every CTA has stored its step-(t-1)
+//     batches up to b + nbx + 1 (refresh_min); that also orders the write-after-read
+//     on the ping-pong buffer (a CTA publishes only after it loaded those patches);
+//   3 dynamic batches with the slab P2P halo stores (the only 2D instantiation that
+//     carries the peer code: it measurably slowed the store path of the others);
+//   4 multi-step dataflow with DYNAMIC ownership: items g = t * nbatch + b are drawn
+//     in order from p.sched; the producer loads item (t, b) once the 3 x 3 batch
+//     neighbourhood has flags[n] >= flag_base + t (its step t-1 stored); the epilogue
+//     publishes flags[b] = flag_base + t + 1 after the item's stores complete (every
+//     kPubEvery items, and whenever it idled 2 us, so no circular wait). Items of
+//     step t depend only on items drawn earlier, and a CTA holds only items it drew,
+//     so the schedule needs no co-residency.
+enum StepMode { kModeStatic = 0, kModeDynamic = 1, kModeMulti = 2, kModePeer = 3, kModeMultiDyn = 4 };
 
 // NS: output staging buffers (TMA stores of batch n read one while batch n + 1 stages
 // into the next; 1 = the epilogue waits for each batch's stores to leave smem)
@@ -231,8 +241,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         Z0 = b / (nbx * nby) + (DIMS == 3 ? p.slow_lo : 0);
     };
     constexpr bool multi = MODE == kModeMulti;
-    // single-step launches with a scheduler counter draw batches dynamically
-    constexpr bool dyn = MODE == kModeDynamic || MODE == kModePeer;
+    constexpr bool mdyn = MODE == kModeMultiDyn;
+    // launches with a scheduler counter draw batches (mdyn: items) dynamically
+    constexpr bool dyn = MODE == kModeDynamic || MODE == kModePeer || mdyn;
+    const int nitems = mdyn ? p.nbatch * p.nsteps : p.nbatch;
+    int32_t* sPub = sBid + kBidSlots;  // mdyn: committed, unpublished items (epilogue etid 0)
     constexpr bool peer = MODE == kModePeer || DIMS == 3;  // (3D whole-window: one instantiation)
     auto next_bid = [&](int r) {  // consumers: batch index of real iteration r (-1: done)
         mbar_wait(&bid_full[r % kBidSlots], (r / kBidSlots) & 1);
@@ -253,26 +266,44 @@ __global__ void __launch_bounds__(kThreads, 1)
             // behind the current batch's wait / issue
             uint32_t nxt = blockIdx.x;
             for (;; ++r) {
-                int b = -1;
+                int g = -1;
                 if (lane == 0) {
-                    b = nxt < static_cast<uint32_t>(p.nbatch) ? static_cast<int>(nxt) : -1;
-                    if (b >= 0) nxt = static_cast<uint32_t>(G) + atomicAdd(p.sched, 1u) - p.sched_base;
-                    sBid[r % kBidSlots] = b;
+                    g = nxt < static_cast<uint32_t>(nitems) ? static_cast<int>(nxt) : -1;
+                    if (g >= 0) nxt = static_cast<uint32_t>(G) + atomicAdd(p.sched, 1u) - p.sched_base;
+                    sBid[r % kBidSlots] = g;
                     mbar_arrive(&bid_full[r % kBidSlots]);
                 }
-                b = __shfl_sync(0xffffffffu, b, 0);
-                if (b < 0) break;
+                g = __shfl_sync(0xffffffffu, g, 0);
+                if (g < 0) break;
+                const int t = mdyn ? g / p.nbatch : 0, b = mdyn ? g - t * p.nbatch : g;
                 int X0, Y0, Z0;
                 batch_coords(b, X0, Y0, Z0);
+                if constexpr (mdyn) {
+                    if (t > 0) {  // lanes 0..8: the 3 x 3 neighbourhood has stored step t - 1
+                        const int by = b / nbx, bx = b - by * nbx;
+                        const int ny = by + static_cast<int>(lane) / 3 - 1, nx = bx + static_cast<int>(lane) % 3 - 1;
+                        const bool mine = lane < 9 && ny >= 0 && ny < nby && nx >= 0 && nx < nbx;
+                        const uint32_t need = p.flag_base + static_cast<uint32_t>(t);
+                        for (;;) {  // acquire loads: no separate fence on the issue path
+                            const bool ok = !mine ||
+                                static_cast<int32_t>(ld_acquire_gpu(p.flags + ny * nbx + nx) - need) >= 0;
+                            if (__all_sync(0xffffffffu, ok)) break;
+                            ++polls;
+                            nanosleep(64);
+                        }
+                        if (lane == 0) fence_proxy_async_global();  // acquired data -> TMA reads
+                    }
+                }
                 if (lane == 0) {
                     const int s = r % NP;
                     mbar_wait(&patch_empty[s], ((r / NP) & 1) ^ 1);
                     mbar_arrive_expect_tx(&patch_full[s], pbytes);
                     void* dst = sP + s * L.p_stride;
+                    const CUtensorMap* tin = &maps.in[(p.src + t) & 1];
                     if (DIMS == 2)
-                        tma_load_2d(dst, &maps.in[p.src & 1], &patch_full[s], X0 + p.load_x0, Y0 + p.load_y0);
+                        tma_load_2d(dst, tin, &patch_full[s], X0 + p.load_x0, Y0 + p.load_y0);
                     else
-                        tma_load_3d(dst, &maps.in[p.src & 1], &patch_full[s], X0 + p.load_x0, Y0, Z0);
+                        tma_load_3d(dst, tin, &patch_full[s], X0 + p.load_x0, Y0, Z0);
                 }
                 __syncwarp();
             }
@@ -406,11 +437,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             st_relaxed_gpu(p.flags + blockIdx.x, p.flag_base + static_cast<uint32_t>(upto));
             published = upto;
         };
+        // mdyn: flags[b] per batch; items [published, committed) wait in sPub
+        auto publish_items = [&](int upto) {
+            fence_proxy_async_global();
+            fence_acq_rel_gpu();
+            for (int i = published; i < upto; ++i) {
+                const int g = sPub[i % kPubRing], tt = g / p.nbatch;
+                st_relaxed_gpu(p.flags + (g - tt * p.nbatch), p.flag_base + static_cast<uint32_t>(tt + 1));
+            }
+            published = upto;
+        };
         for (int j = 0; dyn || j < total; ++j) {
             int t = 0, b, X0, Y0, Z0;
             if constexpr (dyn) {
                 b = next_bid(r);
                 if (b < 0) break;
+                if constexpr (mdyn) {
+                    if (etid == 0) sPub[j % kPubRing] = b;
+                    t = b / p.nbatch;
+                    b -= t * p.nbatch;
+                }
             } else {
                 batch_of(j, t, b);
                 if (b >= p.nbatch) {  // no-op iteration: nothing to store
@@ -429,12 +475,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int i = 0; i < CW; ++i) v[c][i] = 0u;
             } else {
-                if (multi && etid == 0) {  // (multi is constexpr: folded away otherwise)
+                if ((multi || mdyn) && etid == 0) {  // (constexpr: folded away otherwise)
                     const unsigned long long t0 = global_ns();
                     while (!mbar_try_wait(&d_full[s], ph)) {
                         if (published < committed && global_ns() - t0 > 2000ull) {
                             bulk_wait<0>();
-                            publish(committed);
+                            if constexpr (mdyn)
+                                publish_items(committed);
+                            else
+                                publish(committed);
                         }
                     }
                 } else {
@@ -460,10 +509,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 bulk_wait<PUB_LAG>();
                 publish(committed - PUB_LAG);
             }
+            if (mdyn && etid == 0 && committed - published >= kPubEvery + kPubLag) {
+                bulk_wait<kPubLag>();
+                publish_items(committed - kPubLag);
+            }
         }
         if (etid == 0) {
             bulk_wait<0>();  // stores globally complete before the CTA retires
             if (multi) publish(committed);
+            if (mdyn) publish_items(committed);
         }
     }
 

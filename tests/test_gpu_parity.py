@@ -281,8 +281,9 @@ def test_stream_variants_long_runs(gpu):
     assert int(res.stdout.split()[1]) >= 10  # variants that fit the stencil all ran
 
 
-# The multi-step dataflow launch (SST_MULTISTEP=1: one launch, T steps, cross-CTA
-# progress counters) must equal T single-step launches bitwise: same arithmetic per step, so any
+# The multi-step dataflow launches (SST_MULTISTEP=1: one launch, T steps, cross-CTA
+# progress counters; =2: dynamic batch ownership, per-batch flags) must equal T
+# single-step launches bitwise: same arithmetic per step, so any
 # ordering bug (a batch loading a neighbour's halo before it was stored) shows up
 # as a mismatch. Shapes cover grids with fewer batches than SMs, a single batch
 # row or column, ragged edges, and many steps.
@@ -295,7 +296,7 @@ def test_multistep_launch_equals_single_steps(gpu, monkeypatch, name, dims, step
     g = oracle.random_grid(dims, seed=21).astype(np.float32)
 
     def go(multistep, dynamic=True):
-        monkeypatch.setenv("SST_MULTISTEP", "1" if multistep else "0")
+        monkeypatch.setenv("SST_MULTISTEP", str(int(multistep)))
         monkeypatch.setenv("SST_DYN", "1" if dynamic else "0")
         eng = SparseStencil(name, list(dims))
         try:
@@ -305,11 +306,13 @@ def test_multistep_launch_equals_single_steps(gpu, monkeypatch, name, dims, step
         finally:
             eng.close()
 
-    multi, n_multi = go(True)
-    single, n_single = go(False)              # default: dynamic batch scheduling
-    static, _ = go(False, dynamic=False)      # static batch striding
-    assert n_multi == 1 and n_single == steps
+    multi, n_multi = go(1)                    # static batch ownership, per-CTA counters
+    mdyn, n_mdyn = go(2)                      # dynamic ownership, per-batch flags
+    single, n_single = go(0)                  # default: dynamic batch scheduling
+    static, _ = go(0, dynamic=False)          # static batch striding
+    assert n_multi == 1 and n_mdyn == 1 and n_single == steps
     assert np.array_equal(multi, single)
+    assert np.array_equal(mdyn, single)
     assert np.array_equal(static, single)
 
 
