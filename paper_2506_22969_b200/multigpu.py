@@ -212,7 +212,7 @@ class SlabStencil:
             return bytes(h)
 
         mine = {"bufs": [handle(b0.value), handle(b1.value)], "flags": handle(flags.value),
-                "slices": self.layout.local_slices}
+                "slices": self.layout.local_slices, "device": int(self.device)}
         table = [None] * self.layout.world
         dist.all_gather_object(table, mine, group=self.group)
 
@@ -227,6 +227,14 @@ class SlabStencil:
             if not 0 <= nb < self.layout.world:
                 continue
             e = table[nb]
+            # the kernel's TMA stores and the stream flag writes go straight into the
+            # neighbour's memory: its GPU must be peer-accessible (NVLink / NVSwitch)
+            import torch
+
+            if e["device"] != int(self.device) and not torch.cuda.can_device_access_peer(int(self.device),
+                                                                                       e["device"]):
+                raise RuntimeError(f"halo='p2p': GPU {self.device} cannot access peer GPU {e['device']} "
+                                   "(use halo='nccl')")
             pb = [open_(e["bufs"][0]), open_(e["bufs"][1])]
             check(L.sst_plan_set_peer(self.eng._h, which, C.c_void_p(pb[0]), C.c_void_p(pb[1]),
                                       int(e["slices"])))
