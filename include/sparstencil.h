@@ -174,6 +174,11 @@ SST_API sst_status sst_run_steps(sst_plan* plan, int src, uint64_t steps, void* 
  * blocked axis (used by the multi-GPU driver to split interior / boundary
  * work); y1 <= y0 resets to the full interior. */
 SST_API sst_status sst_set_row_window(sst_plan* plan, uint64_t y0, uint64_t y1);
+/* Two row windows [y0, y1) and [y2, y3) in one launch (2D plans; y0 < y1 <= y2 < y3):
+ * the two boundary windows of a slab step after the interior window has run in the
+ * same step (rows between the windows are rewritten with the values that step
+ * already produced). sst_set_row_window resets to one window. */
+SST_API sst_status sst_set_row_windows(sst_plan* plan, uint64_t y0, uint64_t y1, uint64_t y2, uint64_t y3);
 /* ---- slab decomposition with peer-to-peer halos (fused halo exchange) ----
  * sst_plan_set_peer(plan, 0, ...) names the upper neighbour (the rank holding the
  * preceding slices of the slowest axis), 1 the lower one: its two ping-pong

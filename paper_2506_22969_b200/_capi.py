@@ -22,7 +22,7 @@ EXPORTED = [
     "sst_compiled_perm", "sst_compiled_col_origin", "sst_compiled_matrix",
     "sst_compiled_plan_desc", "sst_plan_create", "sst_plan_destroy", "sst_plan_storage",
     "sst_plan_stats_get", "sst_plan_bind", "sst_upload", "sst_download", "sst_run_steps",
-    "sst_set_row_window", "sst_plan_set_trace", "sst_apply_host", "sst_random_grid", "sst_last_error",
+    "sst_set_row_window", "sst_set_row_windows", "sst_plan_set_trace", "sst_apply_host", "sst_random_grid", "sst_last_error",
     "sst_device_count", "sst_version", "sst_run_compile", "sst_compile_result_destroy",
     "sst_compile_result_summary", "sst_compile_result_report", "sst_compile_result_lut", "sst_explore",
     "sst_plan_set_peer", "sst_plan_buffers", "sst_device_alloc", "sst_device_free", "sst_ipc_handle",
@@ -139,6 +139,7 @@ def lib() -> C.CDLL:
         "sst_download": (i32, [P, i32, P, i32, P]),
         "sst_run_steps": (i32, [P, i32, u64, P, C.POINTER(i32)]),
         "sst_set_row_window": (i32, [P, u64, u64]),
+        "sst_set_row_windows": (i32, [P, u64, u64, u64, u64]),
         "sst_plan_set_trace": (i32, [P, P]),
         "sst_apply_host": (i32, [P, P, P, u64]),
         "sst_random_grid": (i32, [i32, C.POINTER(u64), u64, P]),

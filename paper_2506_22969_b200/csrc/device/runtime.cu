@@ -146,7 +146,7 @@ Variant make_variant() {
             if (p.nsteps > 1)
                 return launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMulti, NS>, grid, smem, st,
                                   maps, p, coop);
-            if (p.sched && p.peer_mask)
+            if (p.sched && (p.peer_mask || p.nby1 != p.nby))
                 return launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModePeer, NS>, grid, smem, st,
                                   maps, p, coop);
             if (p.sched)
@@ -264,7 +264,8 @@ struct sst_plan {
     uint32_t flag_base = 0;
     bool tmap_ok = false;
     int64_t map_lo = -1, map_hi = -1;  // row window the output maps were built for
-    int64_t y_lo = 0, y_hi = -1;  // interior row window
+    int64_t y_lo = 0, y_hi = -1;  // interior row window (two windows: their hull)
+    int64_t y_hi1 = 0, y_lo2 = 0;  // two-window launches (2D): first window end, second start
     uint64_t launches = 0;
     int debug_mode = 0;  // SST_DEBUG_MODE (ablation experiments only)
     uint64_t fuse = 1;   // original time steps per launch
@@ -441,7 +442,19 @@ struct sst_plan {
         p.y_end = gy - 2 * r;
         const int bw = img.geo.tiles_x * sst::kTileW, bh = tiles_y * sst::kTileH;
         p.nbx = (gx - 2 * r + bw - 1) / bw;
-        if (dims == 2) {
+        p.nby1 = 0;
+        p.slow_lo2 = 0;
+        if (dims == 2 && y_lo2 > 0 && y_hi > y_lo) {
+            // two windows [slow_lo, hi1) and [lo2, slow_hi): the out maps span the hull; a
+            // first-window batch running past hi1 rewrites rows the preceding interior
+            // launch of the step already wrote, with the same values
+            const int64_t slow = gy - 2 * r;
+            const int32_t hi1 = static_cast<int32_t>(std::min<int64_t>(y_hi1, slow));
+            p.slow_lo2 = static_cast<int32_t>(std::min<int64_t>(y_lo2, slow));
+            p.nby1 = (hi1 - p.slow_lo + bh - 1) / bh;
+            p.nby = p.nby1 + (p.slow_hi - p.slow_lo2 + bh - 1) / bh;
+            p.nbz = 1;
+        } else if (dims == 2) {
             p.nby = (p.slow_hi - p.slow_lo + bh - 1) / bh;
             p.nbz = 1;
         } else {
@@ -449,6 +462,7 @@ struct sst_plan {
             p.nbz = std::max(0, p.slow_hi - p.slow_lo);
         }
         p.nbatch = p.nbx * p.nby * p.nbz;
+        if (p.nby1 == 0) p.nby1 = p.nby;
         p.k_pad = img.geo.k_pad;
         p.nks = static_cast<int32_t>(img.a_smem.size() * 2 / 4096);  // K steps of the A'' image
         p.patch_w = img.geo.patch_w;
@@ -554,7 +568,8 @@ struct sst_plan {
             // (2D P2P halos: only the dynamic-peer instantiation carries the peer stores)
             // (the store-only ablation, debug bit 32, has no producer to draw batches)
             const bool dyn = mdyn || (!multi && variant->multistep && !(debug_mode & 32) &&
-                                      (p.peer_mask != 0 || (dyn_e ? std::atoi(dyn_e) != 0 : p.nbatch >= 8 * grid)));
+                                      (p.peer_mask != 0 || p.nby1 != p.nby ||
+                                       (dyn_e ? std::atoi(dyn_e) != 0 : p.nbatch >= 8 * grid)));
             if (dyn && !d_sched) {
                 ck(cudaMalloc(&d_sched, 4), "cudaMalloc(sched)");
                 ck(cudaMemsetAsync(d_sched, 0, 4, st), "cudaMemsetAsync(sched)");
@@ -1014,6 +1029,22 @@ sst_status sst_set_row_window(sst_plan* plan, uint64_t y0, uint64_t y1) {
         if (!plan) throw std::invalid_argument("null plan");
         plan->y_lo = static_cast<int64_t>(y0);
         plan->y_hi = static_cast<int64_t>(y1);
+        plan->y_hi1 = plan->y_lo2 = 0;
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_set_row_windows(sst_plan* plan, uint64_t y0, uint64_t y1, uint64_t y2, uint64_t y3) {
+    try {
+        if (!plan) throw std::invalid_argument("null plan");
+        if (plan->dims != 2 || plan->fold_n) throw std::invalid_argument("two row windows need a 2D plan");
+        if (!(y0 < y1 && y1 <= y2 && y2 < y3)) throw std::invalid_argument("row windows must be y0 < y1 <= y2 < y3");
+        plan->y_lo = static_cast<int64_t>(y0);
+        plan->y_hi = static_cast<int64_t>(y3);
+        plan->y_hi1 = static_cast<int64_t>(y1);
+        plan->y_lo2 = static_cast<int64_t>(y2);
         return SST_OK;
     } catch (...) {
         return sstc::from_current_exception();

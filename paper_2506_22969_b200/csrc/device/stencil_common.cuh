@@ -55,6 +55,8 @@ struct StepParams {
     int32_t slow_lo, slow_hi;  // window over the slowest axis (y in 2D, z in 3D), interior coords
     int32_t y_end;             // interior rows (gy - 2r)
     int32_t nbx, nby, nbz, nbatch;
+    int32_t nby1, slow_lo2;    // 2D two-window launches (kModePeer): batch rows [nby1, nby) cover the
+                               // second window, starting at row slow_lo2 (nby1 == nby: one window)
     int32_t k_pad;             // B'' rows per MMA pass (per z slice when streaming)
     int32_t nks;               // 32-wide K steps in the A'' image (all slices)
     int32_t patch_w, patch_h, patch_planes;

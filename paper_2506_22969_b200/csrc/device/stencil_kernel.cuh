@@ -130,7 +130,8 @@ __device__ __forceinline__ uint32_t refresh_min(const StepParams& p, uint32_t ne
 //     batches up to b + nbx + 1 (refresh_min); that also orders the write-after-read
 //     on the ping-pong buffer (a CTA publishes only after it loaded those patches);
 //   3 dynamic batches with the slab P2P halo stores (the only 2D instantiation that
-//     carries the peer code: it measurably slowed the store path of the others);
+//     carries the peer code: it measurably slowed the store path of the others), also
+//     the two-window launch of the NCCL slab mode (both boundary windows at once);
 //   4 multi-step dataflow with DYNAMIC ownership: items g = t * nbatch + b are drawn
 //     in order from p.sched; the producer loads item (t, b) once the 3 x 3 batch
 //     neighbourhood has flags[n] >= flag_base + t (its step t-1 stored); the epilogue
@@ -239,6 +240,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         X0 = (b % nbx) * (kTXB * kTileW);
         Y0 = ((b / nbx) % nby) * (TYB * kTileH) + (DIMS == 2 ? p.slow_lo : 0);
         Z0 = b / (nbx * nby) + (DIMS == 3 ? p.slow_lo : 0);
+        if constexpr (DIMS == 2 && MODE == kModePeer) {  // two-window launch: second window
+            const int by = (b / nbx) % nby;
+            if (by >= p.nby1) Y0 = (by - p.nby1) * (TYB * kTileH) + p.slow_lo2;
+        }
     };
     constexpr bool multi = MODE == kModeMulti;
     constexpr bool mdyn = MODE == kModeMultiDyn;

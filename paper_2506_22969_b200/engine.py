@@ -153,6 +153,10 @@ class SparseStencil:
     def set_row_window(self, y0: int, y1: int):
         check(lib().sst_set_row_window(self._h, int(y0), int(y1)))
 
+    def set_row_windows(self, y0: int, y1: int, y2: int, y3: int):
+        """Two row windows [y0, y1) and [y2, y3) in one launch (2D)."""
+        check(lib().sst_set_row_windows(self._h, int(y0), int(y1), int(y2), int(y3)))
+
     def apply_host(self, grid: np.ndarray, steps: int, out: Optional[np.ndarray] = None) -> np.ndarray:
         """Host buffers in, full-size host buffer out (H2D + steps + D2H). Pass
         page-locked arrays (e.g. views of pinned torch tensors) for full PCIe speed."""

@@ -337,9 +337,15 @@ class SlabStencil:
             self.eng.run(self.fuse, src=self.cur, stream=stream)
             for w in works:
                 w.wait()
-            for a, b in self.layout.boundary_windows():
-                self._window(a, b)
+            bw = self.layout.boundary_windows()
+            if len(bw) == 2 and len(self.local_dims) == 2:  # both boundary windows, one launch
+                r = self.layout.r
+                self.eng.set_row_windows(bw[0][0] - r, bw[0][1] - r, bw[1][0] - r, bw[1][1] - r)
                 self.eng.run(self.fuse, src=self.cur, stream=stream)
+            else:
+                for a, b in bw:
+                    self._window(a, b)
+                    self.eng.run(self.fuse, src=self.cur, stream=stream)
             self.cur ^= 1
         self.eng.set_row_window(0, 0)
 

@@ -394,3 +394,38 @@ def test_1d_ring_kept_and_sparse_apply(gpu):
     assert np.array_equal(full[:2], g[:2]) and np.array_equal(full[-2:], g[-2:])  # the ring keeps the input
     out = sparse_apply("Heat-1D", g.astype(np.float64), 3)
     assert out.shape == (n - 6,)
+
+
+# Two row windows in one launch (the NCCL slab mode's boundary windows): after the
+# interior window has run, one launch over [r, 2r) and [n - 2r, n - r) must leave the
+# buffer exactly as one full step does (rows between the windows are rewritten with
+# the values the interior launch produced). Small slabs make the first window's
+# batches run over the second window.
+@pytest.mark.parametrize("name,dims", [("Box-2D9P", (300, 517)), ("Star-2D13P", (90, 140)),
+                                       ("Heat-2D", (40, 1000)), ("Box-2D49P", (200, 300))])
+def test_two_window_launch_equals_full_step(gpu, name, dims):
+    from paper_2506_22969_b200 import InvalidArgument
+
+    g = oracle.random_grid(dims, seed=8).astype(np.float32)
+    eng = SparseStencil(name, list(dims))
+    try:
+        eng.bind()
+        r, n = eng.r, dims[0] - 2 * eng.r
+        eng.upload(g, 0)
+        eng.set_row_window(0, 0)
+        eng.run(1, src=0)
+        full = eng.download(1)
+        eng.upload(g, 0)
+        eng.set_row_window(r, n - r)
+        eng.run(1, src=0)
+        eng.set_row_windows(0, r, n - r, n)
+        launches = eng.stats()["launches"]
+        eng.run(1, src=0)
+        assert eng.stats()["launches"] == launches + 1
+        eng.set_row_window(0, 0)
+        split = eng.download(1)
+        with pytest.raises(InvalidArgument):
+            eng.set_row_windows(5, 3, 7, 9)
+    finally:
+        eng.close()
+    assert np.array_equal(split, full)
