@@ -1,4 +1,6 @@
 """Diagnose the per-step numerics of the f16 sparse tensor-core path."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, oracle
 from paper_2506_22969_b200 import SparseStencil, valid_core
 rng = np.random.default_rng(0)

@@ -1,11 +1,11 @@
 """Small device runs for compute-sanitizer (memcheck / synccheck): every kernel
-family on tiny ragged grids. Usage: compute-sanitizer --tool memcheck python tools/sanitize_smoke.py"""
+family on tiny ragged grids. Usage: compute-sanitizer --tool memcheck python tests/diagnostics/sanitize_smoke.py"""
 import os
 import sys
 
 import numpy as np
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import oracle  # noqa: E402
 from paper_2506_22969_b200 import SparseStencil, valid_core  # noqa: E402
 
