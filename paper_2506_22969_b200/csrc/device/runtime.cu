@@ -196,9 +196,10 @@ const Variant* variants(int& n) {
     static const Variant v[] = {
         // 2D (measured order, tools/ablate.py, after the P2P stores moved to their own
         // instantiation): 0 TMEM-A 8x3 with two staging buffers (Box-2D9P 8192^2 83.4 us,
-        // Heat-2D 4096^2 25.0 vs 25.4 us for one buffer), 1 TMEM-A 8x2 (Star-2D13P
-        // 16384^2: 355 us vs 376 for TMEM-A 4x4), 2 TMEM-A 8x3, 3 TMEM-A 4x4, then smem-A
-        make_variant<2, 8, 3, true, 2>(), make_variant<2, 8, 2, true>(), make_variant<2, 8, 3, true>(),
+        // Heat-2D 4096^2 25.0 vs 25.4 us for one buffer), 1 TMEM-A 8x3 (wider stencils where
+        // the second buffer does not fit: Box-2D9P fused t = 2, 1623 vs 1501 GSt/s with 8x2),
+        // 2 TMEM-A 8x2 (Star-2D13P 16384^2: 355 us vs 376 for TMEM-A 4x4), 3 TMEM-A 4x4, smem-A
+        make_variant<2, 8, 3, true, 2>(), make_variant<2, 8, 3, true>(), make_variant<2, 8, 2, true>(),
         make_variant<2, 4, 4, true>(), make_variant<2, 8, 3, false>(), make_variant<2, 4, 4, false>(),
         make_variant<2, 4, 2, true>(), make_variant<2, 8, 2, false>(), make_variant<2, 4, 2, false>(),
         make_variant<2, 8, 4, false>(),
