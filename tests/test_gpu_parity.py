@@ -190,6 +190,37 @@ def test_full_size_multi_step_windows(gpu):
         assert np.abs(got - want).max() <= tol_abs(steps)
 
 
+@pytest.mark.parametrize("name,dims,edge", [("Box-3D27P", (1024, 1024, 1024), 48),
+                                            ("Star-2D13P", (16384, 16384), 160)])
+def test_full_size_one_step_windows(gpu, name, dims, edge):
+    """The remaining BASELINE.json grids at full size (fp32 input from the engine's
+    generator, no fp64 copy of the whole grid): one step, bit-exact against the oracle
+    on corner, edge and interior windows (one step's output depends only on the window
+    plus an r halo)."""
+    import ctypes as C
+
+    from paper_2506_22969_b200 import lib
+    from paper_2506_22969_b200._capi import check
+
+    g = np.empty(dims, dtype=np.float32)
+    cd = (C.c_uint64 * len(dims))(*dims)
+    check(lib().sst_random_grid(len(dims), cd, 9, g.ctypes.data_as(C.c_void_p)))
+    eng = SparseStencil(name, list(dims))
+    try:
+        r = eng.r
+        out = eng.apply_host(g, 1)
+    finally:
+        eng.close()
+    n = dims[0]
+    for o in (r, n // 2 - edge // 2, n - r - edge):  # same offset on every axis
+        lo = [o] * len(dims)
+        sub = g[tuple(slice(a - r, a + edge + r) for a in lo)].astype(np.float64)
+        want = oracle.direct_apply(name, sub, 1)
+        got = out[tuple(slice(a, a + edge) for a in lo)].astype(np.float64)
+        assert np.array_equal(got, want), (name, o)
+    del out, g
+
+
 @pytest.mark.parametrize("name,fuse", [("Box-2D9P", 2), ("Heat-2D", 3), ("Box-2D9P", 4), ("Box-3D27P", 2),
                                        ("Heat-3D", 2)])
 def test_temporal_fusion(gpu, name, fuse):
