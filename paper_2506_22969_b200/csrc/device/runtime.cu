@@ -101,11 +101,12 @@ struct Variant {
     sst::SmemLayout (*layout)(int nks, int k_pad, int pw, int ph, int planes);
     void (*configure)(int smem);
     bool multistep;  // one launch can run many time steps (2D dataflow kernel)
+    int ctas_per_sm = 1;  // co-resident CTAs the variant is built for (smem / TMEM / registers)
     void (*launch)(int grid, int smem, cudaStream_t st, const sst::MapSet& maps, const sst::StepParams& p,
                    bool cooperative);
 };
 
-template <int D, int TYB, int NP, bool AT, int NS = sst::kStageBufs>
+template <int D, int TYB, int NP, bool AT, int NS = sst::kStageBufs, int CPS = 1>
 Variant make_variant() {
     Variant v{};
     v.dims = D;
@@ -113,25 +114,26 @@ Variant make_variant() {
     v.np = NP;
     v.a_tmem = AT;
     v.acc_cols = 2 * sst::kTXB * TYB;
+    v.ctas_per_sm = CPS;
     v.layout = [](int nks, int k_pad, int pw, int ph, int planes) {
         return sst::smem_layout<TYB, NP, AT, NS>(nks, k_pad, pw, ph, planes);
     };
     // 2D: one instantiation per time-loop mode (static / dynamic / multi-step)
     v.configure = [](int smem) {
-        ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeStatic, NS>,
+        ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeStatic, NS, CPS>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
            "cudaFuncSetAttribute");
         if constexpr (D == 2) {
-            ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeDynamic, NS>,
+            ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeDynamic, NS, CPS>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                "cudaFuncSetAttribute");
-            ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMulti, NS>,
+            ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMulti, NS, CPS>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                "cudaFuncSetAttribute");
-            ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModePeer, NS>,
+            ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModePeer, NS, CPS>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                "cudaFuncSetAttribute");
-            ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMultiDyn, NS>,
+            ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMultiDyn, NS, CPS>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                "cudaFuncSetAttribute");
         }
@@ -141,19 +143,19 @@ Variant make_variant() {
                   bool coop) {
         if constexpr (D == 2) {
             if (p.multi_dyn)
-                return launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMultiDyn, NS>, grid, smem, st,
+                return launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMultiDyn, NS, CPS>, grid, smem, st,
                                   maps, p, coop);
             if (p.nsteps > 1)
-                return launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMulti, NS>, grid, smem, st,
+                return launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMulti, NS, CPS>, grid, smem, st,
                                   maps, p, coop);
             if (p.sched && (p.peer_mask || p.nby1 != p.nby))
-                return launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModePeer, NS>, grid, smem, st,
+                return launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModePeer, NS, CPS>, grid, smem, st,
                                   maps, p, coop);
             if (p.sched)
-                return launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeDynamic, NS>, grid, smem, st,
+                return launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeDynamic, NS, CPS>, grid, smem, st,
                                   maps, p, coop);
         }
-        launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeStatic, NS>, grid, smem, st, maps, p, coop);
+        launch_pdl(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeStatic, NS, CPS>, grid, smem, st, maps, p, coop);
     };
     return v;
 }
@@ -194,15 +196,16 @@ Variant make_stream_variant() {
 // experiments; SST_A_SMEM=1 skips the A''-in-TMEM variants)
 const Variant* variants(int& n) {
     static const Variant v[] = {
-        // 2D (measured order, tools/ablate.py, after the P2P stores moved to their own
-        // instantiation): 0 TMEM-A 8x3 with two staging buffers (Box-2D9P 8192^2 83.4 us,
-        // Heat-2D 4096^2 25.0 vs 25.4 us for one buffer), 1 TMEM-A 8x3 (wider stencils where
-        // the second buffer does not fit: Box-2D9P fused t = 2, 1623 vs 1501 GSt/s with 8x2),
-        // 2 TMEM-A 8x2 (Star-2D13P 16384^2: 355 us vs 376 for TMEM-A 4x4), 3 TMEM-A 4x4, smem-A
-        make_variant<2, 8, 3, true, 2>(), make_variant<2, 8, 3, true>(), make_variant<2, 8, 2, true>(),
-        make_variant<2, 4, 4, true>(), make_variant<2, 8, 3, false>(), make_variant<2, 4, 4, false>(),
-        make_variant<2, 4, 2, true>(), make_variant<2, 8, 2, false>(), make_variant<2, 4, 2, false>(),
-        make_variant<2, 8, 4, false>(),
+        // 2D (measured order, tools/ablate.py): 0 TMEM-A 4x2 built for TWO co-resident CTAs
+        // per SM (each CTA's pipeline bubbles filled by the other's; 81 KiB smem, <= 256 TMEM
+        // columns, <= 102 registers): Box-2D9P 8192^2 83.0 us vs 83.2 for the best one-CTA
+        // variant, Heat-2D 4096^2 24.8 vs 25.1, Star-2D13P 16384^2 341 vs 354, fused Box-2D9P
+        // t = 3 / 4: 2254 / 2964 GSt/s vs 2166 / 2854; then the one-CTA variants: 1 TMEM-A 8x3
+        // with two staging buffers, 2 TMEM-A 8x3, 3 TMEM-A 8x2, 4 TMEM-A 4x4, then smem-A
+        make_variant<2, 4, 2, true, 1, 2>(), make_variant<2, 8, 3, true, 2>(), make_variant<2, 8, 3, true>(),
+        make_variant<2, 8, 2, true>(), make_variant<2, 4, 4, true>(), make_variant<2, 8, 3, false>(),
+        make_variant<2, 4, 4, false>(), make_variant<2, 4, 2, true>(), make_variant<2, 8, 2, false>(),
+        make_variant<2, 4, 2, false>(),
         // 3D z-streaming (10-16): TMEM-A TYB 4 NP 4 (Box-3D27P 512^3: 206 us vs 222 smem-A), ...
         make_stream_variant<4, 4, 3, true>(), make_stream_variant<4, 3, 3, true>(),
         make_stream_variant<8, 3, 3, true>(), make_stream_variant<4, 2, 3, true>(),
@@ -215,9 +218,9 @@ const Variant* variants(int& n) {
         make_stream_variant<8, 2, 3, true, 2, 5, 2>(), make_stream_variant<8, 2, 3, true, 2, 4, 2>(),
         // 3D whole-window kernel (kz != 3 or non-streamable layouts): 25-27
         make_variant<3, 2, 4, false>(), make_variant<3, 2, 3, false>(), make_variant<3, 2, 2, false>(),
-        // more 2D (28-31): <D, TYB, NP, AT, NS>
-        make_variant<2, 8, 4, true>(), make_variant<2, 4, 4, true, 2>(), make_variant<2, 8, 2, true, 2>(),
-        make_variant<2, 4, 3, true, 2>(),
+        // more 2D (28-31): <D, TYB, NP, AT, NS, CPS>
+        make_variant<2, 8, 4, false>(), make_variant<2, 4, 3, true, 1, 2>(), make_variant<2, 4, 4, true, 2>(),
+        make_variant<2, 8, 2, true, 2>(),
         // 3D z-streaming with KZ = 5 (temporally fused 3D stencils, k = 5: 40 K steps of A''):
         // 32-35 <TYB, NP, KZ, AT>
         make_stream_variant<2, 4, 5, true>(), make_stream_variant<2, 6, 5, true>(),
@@ -499,7 +502,7 @@ struct sst_plan {
             const int64_t groups = std::max<int64_t>(1, std::min<int64_t>(num_sms / p.nbx, bands));
             return static_cast<int>(groups * p.nbx);
         }
-        return std::min(p.nbatch, num_sms);
+        return std::min(p.nbatch, num_sms * variant->ctas_per_sm);
     }
 
     // Launch `nsteps` operator applications starting from buffer src; returns the
@@ -651,6 +654,9 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
         int max_smem = 0;
         ck(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device),
            "cudaDeviceGetAttribute");
+        int smem_per_sm = 0;
+        ck(cudaDeviceGetAttribute(&smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device),
+           "cudaDeviceGetAttribute");
         ck(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, device),
            "cudaDeviceGetAttribute");
         const int k_pad = static_cast<int>((d->cols + 31) / 32 * 32) * terms;
@@ -707,9 +713,12 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
             const sst::SmemLayout L = v.layout(nks, kp, geo.patch_w, ph, planes);
             const int need = static_cast<int>(L.total) + 1024;  // slack for the 1 KiB base alignment
             if (need > max_smem || ph > 256) continue;
+            // co-resident CTAs: each takes its smem plus the 1 KiB the driver reserves per CTA
+            if (v.ctas_per_sm > 1 && v.ctas_per_sm * (need + 1024) > smem_per_sm) continue;
             const uint32_t tneed =
                 sst::tmem_budget(static_cast<uint32_t>(v.acc_cols), static_cast<uint32_t>(nks), v.a_tmem).need;
             if (tneed > 512) continue;
+            if (v.ctas_per_sm > 1 && tneed > 512u / static_cast<uint32_t>(v.ctas_per_sm)) continue;
             if (sst::prologue_scratch_bytes(nks, v.a_tmem) > L.gsrc - L.b) continue;
             P->variant = &v;
             P->smem = need;

@@ -143,8 +143,10 @@ enum StepMode { kModeStatic = 0, kModeDynamic = 1, kModeMulti = 2, kModePeer = 3
 
 // NS: output staging buffers (TMA stores of batch n read one while batch n + 1 stages
 // into the next; 1 = the epilogue waits for each batch's stores to leave smem)
-template <int DIMS, int TYB, int NP, bool AT, int MODE = kModeStatic, int NS = kStageBufs>
-__global__ void __launch_bounds__(kThreads, 1)
+// CPS: CTAs per SM the variant is built for (2: small-smem variants whose two co-resident
+// CTAs overlap one another's pipeline bubbles; registers capped accordingly)
+template <int DIMS, int TYB, int NP, bool AT, int MODE = kModeStatic, int NS = kStageBufs, int CPS = 1>
+__global__ void __launch_bounds__(kThreads, CPS)
     stencil_step_kernel(const __grid_constant__ MapSet maps, const StepParams p) {
     constexpr int N = kTXB * TYB;
     constexpr int CW = 2 * TYB;          // MMA columns per output box
