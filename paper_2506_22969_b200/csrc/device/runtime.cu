@@ -120,22 +120,20 @@ Variant make_variant() {
     };
     // 2D: one instantiation per time-loop mode (static / dynamic / multi-step)
     v.configure = [](int smem) {
-        ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeStatic, NS, CPS>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-           "cudaFuncSetAttribute");
+        // max shared-memory carveout: the co-residency the variant is built for (CPS CTAs
+        // per SM) must also hold for the occupancy check of cooperative launches
+        auto setup = [smem](auto kernel) {
+            ck(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+               "cudaFuncSetAttribute");
+            ck(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100),
+               "cudaFuncSetAttribute(carveout)");
+        };
+        setup(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeStatic, NS, CPS>);
         if constexpr (D == 2) {
-            ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeDynamic, NS, CPS>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-               "cudaFuncSetAttribute");
-            ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMulti, NS, CPS>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-               "cudaFuncSetAttribute");
-            ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModePeer, NS, CPS>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-               "cudaFuncSetAttribute");
-            ck(cudaFuncSetAttribute(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMultiDyn, NS, CPS>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-               "cudaFuncSetAttribute");
+            setup(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeDynamic, NS, CPS>);
+            setup(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMulti, NS, CPS>);
+            setup(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModePeer, NS, CPS>);
+            setup(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeMultiDyn, NS, CPS>);
         }
     };
     v.multistep = D == 2;
@@ -496,13 +494,15 @@ struct sst_plan {
 
     // streaming kernels: (row-band groups) x nbx CTAs, see stencil3d_kernel.cuh;
     // the others: persistent CTAs striding over batches
-    int grid_size(const sst::StepParams& p) const {
+    // cooperative: the multi-step launch with static ownership needs every CTA resident;
+    // the driver's occupancy check for cooperative launches admits one CTA per SM here
+    int grid_size(const sst::StepParams& p, bool cooperative = false) const {
         if (variant->kz > 0) {
             const int64_t bands = static_cast<int64_t>(p.nby) * p.nbz;
             const int64_t groups = std::max<int64_t>(1, std::min<int64_t>(num_sms / p.nbx, bands));
             return static_cast<int>(groups * p.nbx);
         }
-        return std::min(p.nbatch, num_sms * variant->ctas_per_sm);
+        return std::min(p.nbatch, num_sms * (cooperative ? 1 : variant->ctas_per_sm));
     }
 
     // Launch `nsteps` operator applications starting from buffer src; returns the
@@ -511,7 +511,6 @@ struct sst_plan {
     int launch(int src, uint64_t nsteps, cudaStream_t st) {
         sst::StepParams p = step_params(src);
         if (p.nbatch <= 0 || nsteps == 0) return src;
-        const int grid = grid_size(p);
         if (p.slow_lo != map_lo || p.slow_hi != map_hi) make_tmaps();  // window changed
         // Default: one launch per step, batches drawn dynamically, PDL overlapping
         // consecutive steps (Box-2D9P 8192^2: 83.4 us/step vs 86.4 for the
@@ -528,6 +527,7 @@ struct sst_plan {
         const bool multi = ms_env && variant->multistep && full && nsteps > 1 && !fold_n && !peer_buf[0][0] &&
                            !peer_buf[1][0];
         const bool mdyn = multi && ms_dyn;
+        const int grid = grid_size(p, multi && !mdyn);
         if (multi && flags_n < p.nbatch) {
             cudaFree(d_flags);
             d_flags = nullptr;
