@@ -19,5 +19,8 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:sten
   -o $out/prof_star2d python bench.py --config star2d --steps 4 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:stencil_step -s 8 -c 1 \
   -o $out/prof_heat2d python bench.py --config heat2d --steps 10 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
-# summaries (run here afterwards): for k in box2d box3d star2d heat2d; do
-#   python tools/ncu_summary.py $out/prof_$k.ncu-rep > profiles/<round>/ncu_${k}_full.txt; done
+# summaries on the box (gpurun copies back at most 64 MiB: the .ncu-rep files would exceed it)
+for k in box2d box3d star2d heat2d; do
+  python tools/ncu_summary.py $out/prof_$k.ncu-rep > $out/ncu_${k}_full.txt 2>&1
+done
+rm -f $out/*.ncu-rep
