@@ -176,6 +176,38 @@ def cpu_baseline(stencil, dims, budget_s=12.0):
                       f"of the {'x'.join(map(str, dims))} grid ({dt:.1f} s)"}
 
 
+def parity_check(stencil, host_in, host_out, steps, r, precision):
+    """The checker (test infrastructure, outside every timed region): windows of
+    the e2e run's output against the CPU oracle — the fp64 reference sweep (rel-L2,
+    max-abs) and, for f16, the round16-iterated oracle (bitwise). An output window
+    needs its input window plus a steps*r halo (tests/test_gpu_baseline_parity.py)."""
+    import oracle
+
+    dims = host_in.shape
+    w = 64 if len(dims) == 2 else 16
+    h = steps * r
+    if any(n < 2 * h + w for n in dims):
+        return None
+    sq_e = sq_r = max_abs = 0.0
+    exact = True
+    t0 = time.perf_counter()
+    for o in ([h] * len(dims), [(n - w) // 2 for n in dims], [n - h - w for n in dims]):
+        src = host_in[tuple(slice(a - h, a + w + h) for a in o)]
+        got = host_out[tuple(slice(a, a + w) for a in o)].astype(np.float64)
+        want = oracle.direct_apply_mt(stencil, src, steps)
+        d = got - want
+        sq_e += float(np.sum(d * d))
+        sq_r += float(np.sum(want * want))
+        max_abs = max(max_abs, float(np.abs(d).max()))
+        if precision == "f16":
+            exact &= bool(np.array_equal(got, oracle.direct_apply_mt(stencil, src, steps, round16=True)))
+    return {"steps": steps, "rel_l2": (sq_e / sq_r) ** 0.5, "max_abs": max_abs,
+            "vs": "fp64 reference sweep (oracle pinned to direct_apply), valid region",
+            "bitwise_round16_semantics": exact if precision == "f16" else None,
+            "windows": f"3 windows of {w}^{len(dims)} outputs (low corner, middle, high corner)",
+            "check_s": time.perf_counter() - t0}
+
+
 def run_reference(args, cfg):
     stencil, dims, tsteps = cfg
     ws, rank, _ = _dist_env()
@@ -319,6 +351,7 @@ def run_engine(args, cfg, cfg_name):
 
     # e2e through the public API from host memory (rank-local slab)
     e2e = None
+    parity = None
     if not args.no_e2e:
         # page-locked host buffers (what a production caller hands the C ABI)
         host_t = torch.empty(tuple(grid.shape), dtype=torch.float32, pin_memory=True)
@@ -342,6 +375,10 @@ def run_engine(args, cfg, cfg_name):
         e2e = {"value": e2e_steps * cells_global / dt / 1e9, "unit": "GStencil/s",
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                "step": f"one sst_apply_host call = H2D + {e2e_steps} time steps + D2H"}
+        if rank == 0 and ws == 1 and not args.no_cpu:
+            # (fused operators round once per launch: a different semantics, not checked here)
+            if args.fuse == 1:
+                parity = parity_check(stencil, host, out_h, e2e_steps, eng.layout.r, args.precision)
 
     if rank != 0:
         if ws > 1:
@@ -377,6 +414,7 @@ def run_engine(args, cfg, cfg_name):
                      else "sst::stencil_step_kernel"},
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "parity": parity,
         "gpu_launches": int(launches),
         "clocks": clk,
     }

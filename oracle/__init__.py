@@ -51,6 +51,8 @@ def orc() -> C.CDLL:
         L.or_preset.restype = i32
         L.or_direct_apply.argtypes = [i32, P, i32, i32, P, P, P, u64, P]
         L.or_direct_apply.restype = i32
+        L.or_direct_apply_mt.argtypes = [i32, P, i32, i32, P, P, P, u64, P, i32, i32]
+        L.or_direct_apply_mt.restype = i32
         _orc = L
     return _orc
 
@@ -118,6 +120,29 @@ def direct_apply(name: str, grid: np.ndarray, steps: int) -> np.ndarray:
                                g.ctypes.data, steps, out.ctypes.data)
     if rc != 0:
         raise RuntimeError(f"or_direct_apply failed ({rc})")
+    return out
+
+
+def direct_apply_mt(name: str, grid: np.ndarray, steps: int, threads: int | None = None,
+                    round16: bool = False) -> np.ndarray:
+    """direct_apply with its output rows split over host threads (bitwise equal to
+    direct_apply). round16=True: the device path's SST_PREC_F16 semantics — every
+    step rounds its inputs to binary16 (RNE), sums exactly (fp64) and stores fp32."""
+    ndims, k, offs, w = preset(name)
+    g = np.ascontiguousarray(grid, dtype=np.float64)
+    if g.ndim != ndims:
+        raise ValueError("grid dimensionality does not match stencil")
+    shape = tuple(n - steps * (k - 1) for n in g.shape)
+    if steps < 1 or any(s < 1 for s in shape):
+        raise ValueError("grid smaller than kernel")
+    out = np.empty(shape, dtype=np.float64)
+    d = _dims(g.shape)
+    offs = np.ascontiguousarray(offs)
+    nt = int(threads or os.cpu_count() or 1)
+    rc = orc().or_direct_apply_mt(ndims, d.ctypes.data, k, len(w), offs.ctypes.data, w.ctypes.data,
+                                  g.ctypes.data, steps, out.ctypes.data, nt, 1 if round16 else 0)
+    if rc != 0:
+        raise RuntimeError(f"or_direct_apply_mt failed ({rc})")
     return out
 
 

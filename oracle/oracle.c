@@ -10,10 +10,18 @@
  *                                         points sorted lexicographically
  *   or_direct_apply  stencil.cpp:231-270  valid region (N - k + 1 per axis per
  *                                         step), fp64, lexicographic point order
+ *   or_direct_apply_mt   the same sweep with its output rows split over host
+ *                        threads (every output is computed exactly as in the
+ *                        serial sweep: bitwise identical), plus the round16
+ *                        semantics of the device path as an option: each step
+ *                        rounds its inputs to binary16 (RNE; fp16.hpp:13-59,
+ *                        emulator.cpp:100-117), sums in fp64 and stores fp32
  * Pinned against the reference itself: tests/golden/direct_apply.npz is written
  * by oracle/make_golden.py from oracle/_ref/libstensor_ref.so (the unmodified
  * reference sources) and tests/test_oracle.py checks this file bit-for-bit.
  */
+#include <math.h>
+#include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -190,6 +198,134 @@ int or_direct_apply(int ndims, const uint64_t* dims, int k, int npts, const int*
     }
     uint64_t m = 1;
     for (int d = 0; d < ndims; ++d) m *= cur[d];
+    memcpy(out, a, m * sizeof(double));
+    free(a);
+    free(b);
+    return 0;
+}
+
+/* ------------------------------------------------- threaded / round16 sweep */
+/* binary16 RNE of a value exactly representable in fp32 (the device rounds its
+ * fp32 grid values with __floats2half2_rn), widened back. Bit arithmetic rather
+ * than _Float16 casts (software conversions without F16C: 10x slower). */
+static double round16(double x) {
+    float f = (float)x;
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    const uint32_t e = (u >> 23) & 0xffu;
+    if (e == 0xffu) return x;                   /* inf / nan */
+    if (e >= 113u) {                            /* binary16 normal range: keep 10 bits */
+        u += 0x0fffu + ((u >> 13) & 1u);        /* round half to even (carries into e) */
+        u &= ~0x1fffu;
+        if (((u >> 23) & 0xffu) > 142u) u = (u & 0x80000000u) | 0x7f800000u; /* > 65504: inf */
+        memcpy(&f, &u, 4);
+        return (double)f;
+    }
+    /* binary16 subnormals: multiples of 2^-24, ties to even (default rounding mode) */
+    return (double)(nearbyintf(f * 16777216.0f) / 16777216.0f);
+}
+
+typedef struct {
+    const uint64_t* id;
+    const uint64_t* od;
+    int npts;
+    const int64_t* rel;
+    const double* w;
+    const double* in;
+    double* out;
+    uint64_t row0, row1; /* output rows (z * od[1] + y) of this worker */
+    int store_f32;
+} sweep_job;
+
+static void* sweep_rows(void* arg) {
+    const sweep_job* j = (const sweep_job*)arg;
+    for (uint64_t row = j->row0; row < j->row1; ++row) {
+        const uint64_t z = row / j->od[1], y = row % j->od[1];
+        const double* src = j->in + (z * j->id[1] + y) * j->id[2];
+        double* dst = j->out + row * j->od[2];
+        for (uint64_t x = 0; x < j->od[2]; ++x) {
+            double acc = 0.0;
+            for (int p = 0; p < j->npts; ++p) acc += j->w[p] * src[x + (uint64_t)j->rel[p]];
+            dst[x] = j->store_f32 == 2 ? round16((double)(float)acc)
+                     : j->store_f32 ? (double)(float)acc : acc;
+        }
+    }
+    return NULL;
+}
+
+/* T valid-region steps over `nthreads` host threads. round16 != 0: every step
+ * rounds its input values to binary16 first and stores its outputs as fp32 (the
+ * operand / storage semantics of the device path, SST_PREC_F16); round16 == 0 is
+ * bitwise identical to or_direct_apply. 0 = ok. */
+int or_direct_apply_mt(int ndims, const uint64_t* dims, int k, int npts, const int* offs, const double* w,
+                       const double* in, uint64_t steps, double* out, int nthreads, int round16_ops) {
+    if (steps == 0 || ndims < 1 || ndims > 3 || npts < 1 || npts > 64) return 1;
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    const int r = (k - 1) / 2;
+    uint64_t cur[3] = {1, 1, 1}, n = 1;
+    for (int a = 0; a < ndims; ++a) {
+        if (dims[a] < (uint64_t)k + (steps - 1) * (uint64_t)(k - 1)) return 2;
+        cur[3 - ndims + a] = dims[a];
+        n *= dims[a];
+    }
+    double* a = (double*)malloc(n * sizeof(double));
+    double* b = (double*)malloc(n * sizeof(double));
+    if (!a || !b) {
+        free(a);
+        free(b);
+        return 3;
+    }
+    memcpy(a, in, n * sizeof(double));
+    pthread_t th[256];
+    sweep_job jobs[256];
+    for (uint64_t s = 0; s < steps; ++s) {
+        uint64_t od[3] = {1, 1, 1}, m = 1;
+        for (int d = 3 - ndims; d < 3; ++d) od[d] = cur[d] - (uint64_t)k + 1;
+        for (int d = 0; d < 3; ++d) m *= cur[d];
+        if (round16_ops && s == 0)  /* later steps' inputs were rounded as they were stored */
+            for (uint64_t i = 0; i < m; ++i) a[i] = round16(a[i]);
+        int64_t rel[64];
+        for (int p = 0; p < npts; ++p) {
+            int o[3] = {0, 0, 0};
+            for (int d = 0; d < ndims; ++d) o[3 - ndims + d] = offs[3 * p + d] + r;
+            rel[p] = ((int64_t)o[0] * (int64_t)cur[1] + o[1]) * (int64_t)cur[2] + o[2];
+        }
+        const uint64_t rows = od[0] * od[1];
+        const int nt = (uint64_t)nthreads < rows ? nthreads : (int)rows;
+        for (int t = 0; t < nt; ++t) {
+            sweep_job* j = &jobs[t];
+            j->id = cur;
+            j->od = od;
+            j->npts = npts;
+            j->rel = rel;
+            j->w = w;
+            j->in = a;
+            j->out = b;
+            j->row0 = rows * (uint64_t)t / (uint64_t)nt;
+            j->row1 = rows * (uint64_t)(t + 1) / (uint64_t)nt;
+            /* round16: store fp32; an input of the next step is stored already rounded */
+            j->store_f32 = round16_ops ? (s + 1 < steps ? 2 : 1) : 0;
+        }
+        int started = 0;
+        for (int t = 1; t < nt; ++t)
+            if (pthread_create(&th[t], NULL, sweep_rows, &jobs[t]) == 0) {
+                ++started;
+            } else {
+                sweep_rows(&jobs[t]); /* no thread: run it here */
+                th[t] = 0;
+            }
+        sweep_rows(&jobs[0]);
+        for (int t = 1; t < nt; ++t)
+            if (th[t]) pthread_join(th[t], NULL);
+        (void)started;
+        for (int d = 3 - ndims; d < 3; ++d) cur[d] -= (uint64_t)k - 1;
+        double* t = a;
+        a = b;
+        b = t;
+    }
+    uint64_t m = 1;
+    for (int d = 0; d < 3; ++d) m *= cur[d];
     memcpy(out, a, m * sizeof(double));
     free(a);
     free(b);

@@ -8,7 +8,9 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -62,6 +64,26 @@ bool pdl_enabled() {
 }
 
 using KernelFn = void (*)(sst::MapSet, sst::StepParams);
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize belongs to a kernel instantiation on a
+// device, not to a plan, and a plan's smem depends on its stencil. So the attribute
+// is only ever raised: lowering it for a narrower stencil would make every later
+// launch of a still-live plan with more smem on the same instantiation fail.
+void raise_smem_attr(KernelFn kernel, int smem) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> configured;
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    std::lock_guard<std::mutex> lock(mu);
+    int& cur = configured[{reinterpret_cast<const void*>(kernel), dev}];
+    if (smem <= cur) return;
+    ck(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "cudaFuncSetAttribute");
+    // max shared-memory carveout: the co-residency a variant is built for (CPS CTAs
+    // per SM) must also hold for the occupancy check of cooperative launches
+    ck(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100),
+       "cudaFuncSetAttribute(carveout)");
+    cur = smem;
+}
 
 // cooperative: a multi-step launch relies on all its CTAs being co-resident
 // (CTAs wait on each other's step flags); the attribute makes that a launch-time
@@ -120,14 +142,7 @@ Variant make_variant() {
     };
     // 2D: one instantiation per time-loop mode (static / dynamic / multi-step)
     v.configure = [](int smem) {
-        // max shared-memory carveout: the co-residency the variant is built for (CPS CTAs
-        // per SM) must also hold for the occupancy check of cooperative launches
-        auto setup = [smem](auto kernel) {
-            ck(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-               "cudaFuncSetAttribute");
-            ck(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100),
-               "cudaFuncSetAttribute(carveout)");
-        };
+        auto setup = [smem](KernelFn kernel) { raise_smem_attr(kernel, smem); };
         setup(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeStatic, NS, CPS>);
         if constexpr (D == 2) {
             setup(sst::stencil_step_kernel<D, TYB, NP, AT, sst::kModeDynamic, NS, CPS>);
@@ -171,12 +186,8 @@ Variant make_stream_variant() {
         return sst::smem_layout_stream<TYB, NP, KZ, NB, NACC, NS, AT>(nks, k_pad, pw, ph);
     };
     v.configure = [](int smem) {
-        ck(cudaFuncSetAttribute(sst::stencil3d_stream_kernel<TYB, NP, KZ, NB, NACC, NS, AT, false>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-           "cudaFuncSetAttribute");
-        ck(cudaFuncSetAttribute(sst::stencil3d_stream_kernel<TYB, NP, KZ, NB, NACC, NS, AT, true>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-           "cudaFuncSetAttribute");
+        raise_smem_attr(sst::stencil3d_stream_kernel<TYB, NP, KZ, NB, NACC, NS, AT, false>, smem);
+        raise_smem_attr(sst::stencil3d_stream_kernel<TYB, NP, KZ, NB, NACC, NS, AT, true>, smem);
     };
     v.multistep = false;
     v.launch = [](int grid, int smem, cudaStream_t st, const sst::MapSet& maps, const sst::StepParams& p,
@@ -489,6 +500,11 @@ struct sst_plan {
             }
         }
         p.trace = trace;
+        if (fold_n && r > 0) {
+            p.fold_ring = d_ring_save;
+            p.fold_nint = static_cast<int64_t>(fold_n) - 2 * r;
+            p.fold_w = static_cast<int32_t>(fold_w);
+        }
         return p;
     }
 
@@ -545,9 +561,9 @@ struct sst_plan {
         }
         int cur = src;
         uint64_t left = nsteps;
-        // fold: the last view row also computes the r right-ring cells (and pad); the
-        // valid core never reads them after step 0 (its dependency cone stays inside
-        // the interior), so they are restored only once the run is over
+        // fold: the last view row's store boxes also cover the r right-ring cells; the
+        // kernel stages their input values (saved here) in place of computed ones, so
+        // the ring is fixed across steps as in 2D / 3D (fold_keep_ring)
         const size_t ring_off = static_cast<size_t>(storage.left_pad + fold_n - r);
         if (fold_n && r > 0) {
             if (!d_ring_save) ck(cudaMalloc(&d_ring_save, static_cast<size_t>(r) * 4), "cudaMalloc(ring)");
@@ -596,9 +612,6 @@ struct sst_plan {
             cur = (cur + static_cast<int>(chunk & 1)) & 1;
             left -= chunk;
         }
-        if (fold_n && r > 0)
-            ck(cudaMemcpyAsync(buf[cur] + ring_off, d_ring_save, static_cast<size_t>(r) * 4,
-                               cudaMemcpyDeviceToDevice, st), "cudaMemcpyAsync(ring restore)");
         return cur;
     }
 };

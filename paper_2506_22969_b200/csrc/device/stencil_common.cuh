@@ -79,6 +79,9 @@ struct StepParams {
     uint32_t sched_base;       // counter value at launch start
     int32_t multi_dyn;         // 2D: the multi-step launch with dynamic batch ownership (kModeMultiDyn)
     unsigned long long* trace; // profiling only (sst_plan_set_trace): per CTA {smid, t_start, t_main, t_end}
+    const float* fold_ring;    // 1D fold: the r right-ring cells' input values (else null)
+    int64_t fold_nint;         // 1D fold: interior cells n_int = N - 2r (ring at [n_int, n_int + r))
+    int32_t fold_w;            // 1D fold: interior cells per view row
 };
 
 __device__ __forceinline__ float* buf_of(const StepParams& p, int i) {
@@ -340,6 +343,25 @@ __device__ __forceinline__ void peer_right_edge(const StepParams& p, uint32_t st
         if (to_up) up[off + p.peer_up_shift * p.row_pitch] = val;
         if (to_down) down[off + p.peer_down_shift * p.row_pitch] = val;
     }
+}
+
+// 1D fold: the last view row's store boxes also cover the r right-ring cells
+// [n_int, n_int + r) of the 1D grid (TMA cannot clip inside a row of the view). They
+// keep their input values: staged in place of the computed ones from the copy the
+// plan saved before the run, so every step leaves the ring as it found it.
+template <int TYB>
+__device__ __forceinline__ void fold_keep_ring(const StepParams& p, uint32_t (&v)[kTXB / 2][2 * TYB], int X0,
+                                               int Y0, uint32_t q, uint32_t lane) {
+    const int yr = static_cast<int>(p.fold_nint / p.fold_w), xr = static_cast<int>(p.fold_nint % p.fold_w);
+    if (yr < Y0 || yr >= Y0 + TYB * kTileH || xr + p.r <= X0 || xr >= X0 + kTXB * kTileW) return;
+    const int dx = static_cast<int>(q) * 4 + static_cast<int>(lane / 8), dy = static_cast<int>(lane % 8);
+#pragma unroll
+    for (int c = 0; c < kTXB / 2; ++c)
+#pragma unroll
+        for (int i = 0; i < 2 * TYB; ++i) {
+            const int x = X0 + c * kBoxW + (i & 1) * kTileW + dx, y = Y0 + (i / 2) * kTileH + dy;
+            if (y == yr && x >= xr && x < xr + p.r && x < p.fold_w) v[c][i] = __float_as_uint(p.fold_ring[x - xr]);
+        }
 }
 
 // Right-edge handling of store_batch:

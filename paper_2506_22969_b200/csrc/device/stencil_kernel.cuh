@@ -9,8 +9,9 @@
 //   warps 2-5   gather: B''[q, tile] = patch[tile_origin + koff[q]] (the
 //               memory map of layout.cpp:162-188), fp32 -> fp16 (RNE, the
 //               reference round16 rounding), into the UMMA MN-major operand
-//   warp 1      MMA issuer: tcgen05.mma.sp.cta_group::1.kind::f16, A'' from
-//               smem (compressed, K-major), metadata from TMEM, D in TMEM
+//   warp 1      MMA issuer: tcgen05.mma.sp.cta_group::1.kind::f16, compressed
+//               A'' from TMEM (the default AT variants; K-major smem in the
+//               AT = false ones), metadata from TMEM, D in TMEM
 //   warps 6-9   epilogue: tcgen05.ld -> 128B-swizzled smem staging -> TMA
 //               bulk store through a tensor map clipped to the interior
 //
@@ -502,6 +503,8 @@ __global__ void __launch_bounds__(kThreads, CPS)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&d_empty[s]);
             }
+            if constexpr (DIMS == 2)
+                if (p.fold_ring != nullptr) fold_keep_ring<TYB>(p, v, X0, Y0, q, lane);
             if (!(p.debug_mode & 1))
             {
                 const int par = (p.src + t + 1) & 1;

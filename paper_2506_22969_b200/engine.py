@@ -102,10 +102,12 @@ class SparseStencil:
         self.compiled = stencil if isinstance(stencil, Compiled) else Compiled(
             stencil, grid_dims, r1, r2, fuse)
         self.grid_dims = self.compiled.grid_dims
-        self.fuse = max(1, int(fuse)) if not isinstance(stencil, Compiled) else 1
+        desc = self.compiled.plan_desc()
+        # the fusion factor the operator was compiled with (a pre-compiled Compiled
+        # carries its own; the plan advances that many time steps per launch)
+        self.fuse = max(1, int(desc.fuse))
         self.k = int(self.compiled.info["k"])       # of the (possibly fused) operator
         self.r = (self.k - 1) // 2 // self.fuse     # radius of one original time step
-        desc = self.compiled.plan_desc()
         desc.precision = PRECISIONS[precision]
         self.precision = precision
         h = C.c_void_p()

@@ -287,6 +287,9 @@ class SlabStencil:
         return torch.from_numpy(host).to(torch.device("cuda", self.device))
 
     def load(self, grid):
+        # P2P: a neighbour's last launch may still TMA-store halo slices into this
+        # rank's buffers; every rank's device must be idle before the upload too
+        self._p2p_fence()
         self.eng.upload(grid, which=0)
         self._p2p_fence()
         self.cur = 0
@@ -355,6 +358,7 @@ class SlabStencil:
             return self.eng.apply_host(host, steps, out=out)
         import torch
 
+        self._p2p_fence()  # neighbours' late halo stores land before the upload
         self.eng.upload(np.ascontiguousarray(host, dtype=np.float32), which=0)
         self._p2p_fence()
         self.cur = 0

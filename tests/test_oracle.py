@@ -54,3 +54,51 @@ def test_oracle_matches_reference_live():
         assert np.array_equal(oracle.direct_apply(name, g, 2), oracle.ref_direct_apply(name, g, 2))
         assert np.array_equal(oracle.ref_direct_apply_slabs(name, g, 3),
                               oracle.ref_direct_apply(name, g, 1))
+
+
+@pytest.mark.parametrize("name,dims,steps", [("Heat-2D", (61, 70), 5), ("Box-3D27P", (13, 15, 17), 3),
+                                             ("Star-2D13P", (50, 47), 2), ("1D5P", (300,), 7)])
+def test_threaded_oracle_equals_serial(name, dims, steps):
+    g = oracle.random_grid(dims, seed=11)
+    want = oracle.direct_apply(name, g, steps)
+    for threads in (1, 3, 8):
+        assert np.array_equal(oracle.direct_apply_mt(name, g, steps, threads), want)
+
+
+@pytest.mark.parametrize("name,dims,steps", [("Heat-2D", (40, 50), 6), ("Box-3D27P", (12, 13, 14), 3)])
+def test_round16_oracle_equals_numpy_iteration(name, dims, steps):
+    # round16 semantics of the device path: binary16 RNE operands, exact sum, fp32 storage
+    g = oracle.random_grid(dims, seed=12)
+    cur = g
+    for _ in range(steps):
+        cur = oracle.direct_apply(name, cur.astype(np.float16).astype(np.float64), 1)
+        cur = cur.astype(np.float32).astype(np.float64)
+    assert np.array_equal(oracle.direct_apply_mt(name, g, steps, 4, round16=True), cur)
+
+
+def test_round16_ties_to_even():
+    # binary16 RNE at the halfway points (the oracle's rounding is numpy's / the device's)
+    vals = np.array([1 + 2.0 ** -11, 1 + 3 * 2.0 ** -11, 0.5 + 2.0 ** -12, 2.0 ** -14 * 1.5,
+                     0.99951171875 + 2.0 ** -12], dtype=np.float64)
+    g = np.zeros((1, 3 + len(vals) + 2))
+    g[0, 3:3 + len(vals)] = vals
+    g = np.repeat(g, 3, axis=0)
+    got = oracle.direct_apply_mt("Heat-2D", g, 1, 2, round16=True)
+    want = oracle.direct_apply("Heat-2D", g.astype(np.float16).astype(np.float64), 1)
+    assert np.array_equal(got, want.astype(np.float32).astype(np.float64))
+
+
+def test_round16_bits_match_numpy():
+    # Heat-1D over isolated values: out = 0.5 * round16(v) exactly, so the oracle's
+    # bit-level binary16 RNE is checked against numpy's on normals, subnormals,
+    # halfway cases and overflow
+    rng = np.random.default_rng(0)
+    v = (rng.random(30000) * 2.0 ** rng.integers(-26, 17, 30000)).astype(np.float32).astype(np.float64)
+    v = np.concatenate([v, [65504.0, 65519.99, 65520.0, 70000.0, 2.0 ** -25, 3 * 2.0 ** -25,
+                            1.5 * 2.0 ** -24, 1 + 2.0 ** -11, 1 + 3 * 2.0 ** -11]])
+    g = np.zeros(3 * len(v) + 2)
+    g[1::3][:len(v)] = v
+    out = oracle.direct_apply_mt("Heat-1D", g, 1, 2, round16=True)  # out[i] centred on g[i + 1]
+    got = 2.0 * out[0::3][:len(v)]
+    want = v.astype(np.float16).astype(np.float64)
+    assert np.array_equal(got, want)
