@@ -152,6 +152,12 @@ typedef struct sst_plan_stats {
     int32_t patch_stages;  /* depth of the TMA patch ring */
     int32_t smem_bytes, ctas, batches;
     uint64_t launches;     /* kernel launches issued by this plan so far */
+    uint64_t h16_launches; /* of those, launches reading or writing binary16 inter-step storage
+                              (SST_PREC_F16 runs of >= 2 steps keep steps 1..T-1 in binary16:
+                              the next gather rounds to binary16 RNE anyway, so the result is
+                              bitwise the fp32-storage one at 4 B instead of 8 B per update) */
+    int32_t h16_capable;   /* the plan can run binary16 inter-step storage */
+    int32_t h16_patch_stages; /* binary16 kernels: 100 x patch ring depth + 10 x B operand stages + accumulator stages */
 } sst_plan_stats;
 SST_API sst_status sst_plan_stats_get(const sst_plan* plan, sst_plan_stats* s);
 

@@ -88,7 +88,8 @@ class PlanStats(C.Structure):
                 ("patch_planes", C.c_int32), ("worst_bank_conflict", C.c_int32),
                 ("patch_stages", C.c_int32),
                 ("smem_bytes", C.c_int32), ("ctas", C.c_int32), ("batches", C.c_int32),
-                ("launches", C.c_uint64)]
+                ("launches", C.c_uint64), ("h16_launches", C.c_uint64), ("h16_capable", C.c_int32),
+                ("h16_patch_stages", C.c_int32)]
 
 
 class CompileRequest(C.Structure):

@@ -50,18 +50,25 @@ def _run(cmd, verbose):
 
 
 def build(verbose: bool = False, force: bool = False) -> Path:
+    from concurrent.futures import ThreadPoolExecutor
+
     OBJ.mkdir(exist_ok=True)
-    objs = []
+    objs, jobs = [], []
     for src in HOST_SRCS:
         o = OBJ / (src.stem + ".o")
         objs.append(o)
         if force or _stale(o, [src, *HEADERS, __file__]):
-            _run([CXX, *CXXFLAGS, *INCLUDES, "-c", src, "-o", o], verbose)
+            jobs.append([CXX, *CXXFLAGS, *INCLUDES, "-c", src, "-o", o])
     for src in DEVICE_SRCS:
         o = OBJ / (src.stem + ".cu.o")
         objs.append(o)
         if force or _stale(o, [src, *HEADERS, __file__]):
-            _run([NVCC, *NVFLAGS, *INCLUDES, "-c", src, "-o", o], verbose)
+            jobs.append([NVCC, *NVFLAGS, *INCLUDES, "-c", src, "-o", o])
+    # the translation units compile independently (the kernel instantiations dominate)
+    jobs.sort(key=lambda c: c[0] != NVCC)  # longest first
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for f in [ex.submit(_run, c, verbose) for c in jobs]:
+            f.result()
     if force or _stale(LIB, objs):
         _run([NVCC, "-shared", *ARCH, "-cudart", "static", "-o", LIB, *objs], verbose)
     # the CLI (reference tools/main.cpp) links the same objects statically

@@ -17,6 +17,7 @@
 #include "../host/capi_internal.hpp"
 #include "sparstencil.h"
 #include "stencil3d_kernel.cuh"
+#include "launch_util.cuh"
 #include "stencil_kernel.cuh"
 #include "stensor/device_image.hpp"
 #include "stensor/morph.hpp"
@@ -25,12 +26,7 @@ namespace {
 
 using sstc::CudaError;
 
-void ck(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) {
-        const bool nodev = e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver;
-        throw CudaError(std::string(what) + ": " + cudaGetErrorString(e), nodev);
-    }
-}
+using namespace sstl;
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -51,67 +47,6 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// Every step kernel is launched with programmatic stream serialization: its
-// prologue (barrier init, TMEM alloc, constant staging) runs while the previous
-// step drains, and griddepcontrol.wait in the kernel orders all grid-buffer
-// accesses after that step completes. SST_PDL=0 disables it (A/B experiments).
-bool pdl_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("SST_PDL");
-        return !(e && std::atoi(e) == 0);
-    }();
-    return on;
-}
-
-using KernelFn = void (*)(sst::MapSet, sst::StepParams);
-
-// cudaFuncAttributeMaxDynamicSharedMemorySize belongs to a kernel instantiation on a
-// device, not to a plan, and a plan's smem depends on its stencil. So the attribute
-// is only ever raised: lowering it for a narrower stencil would make every later
-// launch of a still-live plan with more smem on the same instantiation fail.
-void raise_smem_attr(KernelFn kernel, int smem) {
-    static std::mutex mu;
-    static std::map<std::pair<const void*, int>, int> configured;
-    int dev = 0;
-    ck(cudaGetDevice(&dev), "cudaGetDevice");
-    std::lock_guard<std::mutex> lock(mu);
-    int& cur = configured[{reinterpret_cast<const void*>(kernel), dev}];
-    if (smem <= cur) return;
-    ck(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "cudaFuncSetAttribute");
-    // max shared-memory carveout: the co-residency a variant is built for (CPS CTAs
-    // per SM) must also hold for the occupancy check of cooperative launches
-    ck(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100),
-       "cudaFuncSetAttribute(carveout)");
-    cur = smem;
-}
-
-// cooperative: a multi-step launch relies on all its CTAs being co-resident
-// (CTAs wait on each other's step flags); the attribute makes that a launch-time
-// guarantee instead of an assumption.
-void launch_pdl(KernelFn fn, int grid, int smem, cudaStream_t st, const sst::MapSet& maps,
-                const sst::StepParams& p, bool cooperative) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(static_cast<unsigned>(grid));
-    cfg.blockDim = dim3(sst::kThreads);
-    cfg.dynamicSmemBytes = static_cast<size_t>(smem);
-    cfg.stream = st;
-    cudaLaunchAttribute attr[2];
-    int na = 0;
-    if (pdl_enabled()) {
-        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[na].val.programmaticStreamSerializationAllowed = 1;
-        ++na;
-    }
-    if (cooperative) {
-        attr[na].id = cudaLaunchAttributeCooperative;
-        attr[na].val.cooperative = 1;
-        ++na;
-    }
-    cfg.attrs = attr;
-    cfg.numAttrs = static_cast<unsigned>(na);
-    ck(cudaLaunchKernelEx(&cfg, fn, maps, p), "cudaLaunchKernelEx");
-}
-
 // One compiled instantiation of the step kernel: (dims, tile rows per batch,
 // patch pipeline depth, A'' in TMEM or smem). Plans pick the first variant in
 // preference order whose smem and TMEM budgets fit.
@@ -126,6 +61,7 @@ struct Variant {
     int ctas_per_sm = 1;  // co-resident CTAs the variant is built for (smem / TMEM / registers)
     void (*launch)(int grid, int smem, cudaStream_t st, const sst::MapSet& maps, const sst::StepParams& p,
                    bool cooperative);
+    std::vector<sstl::TypedFns> h16c;  // binary16 inter-step storage instantiations (step_h16.cu), if any
 };
 
 template <int D, int TYB, int NP, bool AT, int NS = sst::kStageBufs, int CPS = 1>
@@ -152,6 +88,7 @@ Variant make_variant() {
         }
     };
     v.multistep = D == 2;
+    if constexpr (D == 2) v.h16c = sstl::typed_fns_2d(TYB, NP, AT, NS, CPS);
     v.launch = [](int grid, int smem, cudaStream_t st, const sst::MapSet& maps, const sst::StepParams& p,
                   bool coop) {
         if constexpr (D == 2) {
@@ -241,6 +178,46 @@ const Variant* variants(int& n) {
 
 }  // namespace
 
+namespace {
+// One warp per storage row: rows of the boundary ring (and, in 3D, whole ring
+// planes) are converted in full, other rows only in their r left / right ring cells.
+__global__ void ring_to_half_kernel(const float* src, __half* d0, __half* d1, int gx, int gy, int gz, int r,
+                                    long long rp, long long pp, int lp, long long rph, long long pph, int lph) {
+    const long long rows = static_cast<long long>(gy) * gz;
+    const int lane = static_cast<int>(threadIdx.x & 31);
+    const long long wstride = static_cast<long long>(gridDim.x) * blockDim.x / 32;
+    for (long long row = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; row < rows;
+         row += wstride) {
+        const int z = static_cast<int>(row / gy), y = static_cast<int>(row % gy);
+        const bool full = y < r || y >= gy - r || (gz > 1 && (z < r || z >= gz - r));
+        const float* s = src + z * pp + y * rp + lp;
+        __half* a = d0 + z * pph + y * rph + lph;
+        __half* b = d1 + z * pph + y * rph + lph;
+        if (full) {
+            for (int x = lane; x < gx; x += 32) {
+                const __half h = __float2half_rn(s[x]);
+                a[x] = h;
+                b[x] = h;
+            }
+        } else {
+            for (int i = lane; i < 2 * r; i += 32) {
+                const int x = i < r ? i : gx - 2 * r + i;
+                const __half h = __float2half_rn(s[x]);
+                a[x] = h;
+                b[x] = h;
+            }
+        }
+    }
+}
+}  // namespace
+
+void sstl::launch_ring_to_half(const float* src, __half* d0, __half* d1, int gx, int gy, int gz, int r, long long rp,
+                               long long pp, int lp, long long rph, long long pph, int lph, cudaStream_t st) {
+    const long long rows = static_cast<long long>(gy) * gz;
+    const int blocks = static_cast<int>(std::min<long long>((rows + 7) / 8, 148LL * 16));
+    ring_to_half_kernel<<<blocks, 256, 0, st>>>(src, d0, d1, gx, gy, gz, r, rp, pp, lp, rph, pph, lph);
+}
+
 struct sst_plan {
     int device = 0;
     int dims = 2, k = 3, r = 1;
@@ -290,6 +267,23 @@ struct sst_plan {
     sst::PeerMaps* d_peer_maps = nullptr;
     uint64_t peer_slices[2] = {0, 0};
     float* d_ring_save = nullptr;     // fold: the r right-ring cells, restored after a run
+    // binary16 inter-step storage (SST_PREC_F16 runs of >= 2 steps, full window, no
+    // peers / fold): steps 1 .. T-1 live in hbuf (ring: the f32 ring rounded once per
+    // run), the last step writes the f32 buffer. img_h: gather tables for f16 patches.
+    bool h16_ok = false;              // plan / variant support it
+    sstl::TypedFns h16{};             // the chosen binary16 instantiations
+    int smem_h = 0, smem_f32_h = 0;   // dynamic smem of the binary16-input / fp32-input typed kernels
+    int occ_smem = 0;                 // smem floor keeping CTAs per SM within the TMEM budget
+    int tmem_cols_h = 0;              // TMEM allocation of the typed kernels
+    stensor::DeviceImage img_h;
+    int32_t* d_gsrc_h = nullptr;
+    int32_t* d_gdst_h = nullptr;
+    sst_storage storage_h{};
+    int load_x0_h = 0;
+    __half* hbuf[2] = {nullptr, nullptr};
+    CUtensorMap hin[2]{}, hout[2]{};  // f16 patch loads / interior stores
+    bool hmaps_ok = false;
+    uint64_t h16_launches = 0;        // launches that read or wrote binary16 storage
 
     ~sst_plan() {
         cudaSetDevice(device);
@@ -301,6 +295,10 @@ struct sst_plan {
         cudaFree(d_sched);
         cudaFree(d_ring_save);
         cudaFree(d_peer_maps);
+        cudaFree(d_gsrc_h);
+        cudaFree(d_gdst_h);
+        cudaFree(hbuf[0]);
+        cudaFree(hbuf[1]);
         if (owns_buf) {
             cudaFree(alloc_base[0]);
             cudaFree(alloc_base[1]);
@@ -320,9 +318,10 @@ struct sst_plan {
     }
 
     static void encode(CUtensorMap* m, int rank, void* base, const cuuint64_t* dim,
-                       const cuuint64_t* stride, const cuuint32_t* box, CUtensorMapSwizzle swz) {
+                       const cuuint64_t* stride, const cuuint32_t* box, CUtensorMapSwizzle swz,
+                       CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32) {
         cuuint32_t estride[3] = {1, 1, 1};
-        const CUresult rc = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, static_cast<cuuint32_t>(rank),
+        const CUresult rc = encode_fn()(m, dt, static_cast<cuuint32_t>(rank),
                                         base, dim, stride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                         swz, l2_promotion(),
                                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -508,6 +507,96 @@ struct sst_plan {
         return p;
     }
 
+    // SST_H16=0 keeps fp32 storage between steps (A/B experiments, tests; read per call)
+    static bool h16_enabled() {
+        const char* e = std::getenv("SST_H16");
+        return !(e && std::atoi(e) == 0);
+    }
+
+    // binary16 storage buffers and their tensor maps (allocated on first use)
+    void ensure_h16() {
+        if (hmaps_ok) return;
+        const size_t bytes = storage_h.bytes;
+        for (int i = 0; i < 2; ++i) {
+            if (!hbuf[i]) {
+                ck(cudaMalloc(&hbuf[i], bytes), "cudaMalloc(f16 grid)");
+                ck(cudaMemset(hbuf[i], 0, bytes), "cudaMemset(f16 grid)");
+            }
+        }
+        const cuuint64_t gstride[2] = {storage_h.row_pitch * 2, storage_h.plane_pitch * 2};
+        const int ox = gx - 2 * r, ox8 = ox & ~7;
+        for (int i = 0; i < 2; ++i) {
+            const cuuint64_t gdim[3] = {storage_h.row_pitch, static_cast<cuuint64_t>(gy), static_cast<cuuint64_t>(gz)};
+            const cuuint32_t box[3] = {static_cast<cuuint32_t>(img_h.geo.patch_w),
+                                       static_cast<cuuint32_t>(img_h.geo.patch_h),
+                                       static_cast<cuuint32_t>(img_h.geo.patch_planes)};
+            encode(&hin[i], dims, hbuf[i], gdim, gstride, box, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+            __half* base = hbuf[i] + (dims == 3 ? r * static_cast<int64_t>(storage_h.plane_pitch) : 0) +
+                           static_cast<int64_t>(r) * static_cast<int64_t>(storage_h.row_pitch) +
+                           static_cast<int64_t>(storage_h.left_pad) + r;
+            const cuuint64_t odim[3] = {static_cast<cuuint64_t>(std::max(ox8, 8)),
+                                        static_cast<cuuint64_t>(gy - 2 * r), static_cast<cuuint64_t>(gz - 2 * r)};
+            const cuuint32_t obox[3] = {64u, static_cast<cuuint32_t>(tiles_y * sst::kTileH), 1u};
+            encode(&hout[i], dims, base, odim, gstride, obox, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+        }
+        hmaps_ok = true;
+    }
+
+    // A run of nsteps >= 2 with binary16 inter-step storage: f32 buf[src] -> hbuf[0]
+    // -> hbuf[1] -> ... -> f32 buf[(src + nsteps) & 1] (the index plain ping-pong
+    // would end on; when that is buf[src] itself, step 1 read it long before).
+    int launch_h16(int src, uint64_t nsteps, cudaStream_t st) {
+        ensure_h16();
+        sstl::launch_ring_to_half(buf[src], hbuf[0], hbuf[1], gx, gy, gz, r,
+                                  static_cast<long long>(storage.row_pitch), static_cast<long long>(storage.plane_pitch),
+                                  static_cast<int>(storage.left_pad), static_cast<long long>(storage_h.row_pitch),
+                                  static_cast<long long>(storage_h.plane_pitch), static_cast<int>(storage_h.left_pad),
+                                  st);
+        ck(cudaGetLastError(), "ring_to_half launch");
+        const int fin = static_cast<int>((static_cast<uint64_t>(src) + nsteps) & 1);
+        for (uint64_t t = 0; t < nsteps; ++t) {
+            const bool hi = t > 0, ho = t + 1 < nsteps;
+            sst::StepParams p = step_params(src);
+            const int grid = grid_size(p);
+            sst::MapSet m{};
+            m.in[0] = m.in[1] = hi ? hin[(t - 1) & 1] : maps.in[src];
+            m.out[0] = m.out[1] = ho ? hout[t & 1] : maps.out[fin];
+            float* outp = ho ? reinterpret_cast<float*>(hbuf[t & 1]) : buf[fin];
+            p.src = 0;
+            p.buf[0] = p.buf[1] = outp;
+            p.tmem_cols = tmem_cols_h;
+            if (ho) {
+                p.row_pitch = static_cast<int64_t>(storage_h.row_pitch);
+                p.plane_pitch = static_cast<int64_t>(storage_h.plane_pitch);
+                p.left_pad = static_cast<int32_t>(storage_h.left_pad);
+            }
+            if (hi) {
+                p.load_x0 = load_x0_h;
+                p.patch_w = img_h.geo.patch_w;
+                p.gsrc = d_gsrc_h;
+                p.gdst = d_gdst_h;
+            }
+            const char* dyn_e = std::getenv("SST_DYN");
+            // (the store-only ablation, debug bit 32, has no producer to draw batches)
+            const bool dyn = !(debug_mode & 32) && (dyn_e ? std::atoi(dyn_e) != 0 : p.nbatch >= 8 * grid);
+            if (dyn && !d_sched) {
+                ck(cudaMalloc(&d_sched, 4), "cudaMalloc(sched)");
+                ck(cudaMemsetAsync(d_sched, 0, 4, st), "cudaMemsetAsync(sched)");
+                sched_base = 0;
+            }
+            p.sched = dyn ? d_sched : nullptr;
+            p.sched_base = sched_base;
+            h16.launch(dyn, hi, ho, grid, hi ? smem_h : smem_f32_h, st, m, p);
+            if (dyn) sched_base += static_cast<uint32_t>(p.nbatch + grid * (sst::kDrawAhead - 1));
+            ck(cudaGetLastError(), "kernel launch");
+            ++launches;
+            ++h16_launches;
+        }
+        return fin;
+    }
+
     // streaming kernels: (row-band groups) x nbx CTAs, see stencil3d_kernel.cuh;
     // the others: persistent CTAs striding over batches
     // cooperative: the multi-step launch with static ownership needs every CTA resident;
@@ -543,6 +632,8 @@ struct sst_plan {
         const bool multi = ms_env && variant->multistep && full && nsteps > 1 && !fold_n && !peer_buf[0][0] &&
                            !peer_buf[1][0];
         const bool mdyn = multi && ms_dyn;
+        if (h16_ok && h16_enabled() && !multi && full && nsteps > 1 && !peer_buf[0][0] && !peer_buf[1][0])
+            return launch_h16(src, nsteps, st);
         const int grid = grid_size(p, multi && !mdyn);
         if (multi && flags_n < p.nbatch) {
             cudaFree(d_flags);
@@ -600,7 +691,8 @@ struct sst_plan {
             p.multi_dyn = mdyn ? 1 : 0;
             variant->launch(grid, smem, st, maps, p, multi && !mdyn);
             // (items - grid draws, plus one final draw per CTA)
-            if (dyn) sched_base += static_cast<uint32_t>(p.nbatch * (mdyn ? chunk : 1));
+            if (dyn)
+                sched_base += static_cast<uint32_t>(p.nbatch * (mdyn ? chunk : 1) + grid * (sst::kDrawAhead - 1));
             ck(cudaGetLastError(), "kernel launch");
             ++launches;
             if (mdyn) {  // per-batch step counters
@@ -745,6 +837,16 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
         }
         if (!P->variant)
             throw std::invalid_argument("stencil too wide for one CTA's shared memory");
+        // Occupancy guard: a CTA that finds no free TMEM blocks in tcgen05.alloc until a
+        // co-resident CTA retires — for a persistent CTA holding its first batch, the end
+        // of the launch. So never let more CTAs share an SM than its 512 TMEM columns
+        // hold: pad the dynamic smem instead (binary16 patches made the typed kernels
+        // small enough for a third CTA per SM: Box-2D9P 78 -> 127 us per step).
+        P->occ_smem = [&] {
+            const int allowed = std::max(P->variant->ctas_per_sm, 512 / P->tmem_cols);
+            return std::min(max_smem, smem_per_sm / (allowed + 1));
+        }();
+        P->smem = std::max(P->smem, P->occ_smem);
         P->tiles_y = geo.tiles_y;
         P->img = stensor::build_device_image(geo, d->rows, d->cols, d->a_values, d->a_meta,
                                              origin.data(), d->window_w, d->window_h);
@@ -772,6 +874,53 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
             P->storage.bytes = (cells + 3) / 4 * 4 * 4;
         }
 
+        // binary16 inter-step storage: f16 operands only, 2D full-grid runs (see launch)
+        if (terms == 1 && !P->fold_n && !P->variant->h16c.empty()) {
+            const uint64_t lph = (8 - static_cast<uint64_t>(P->r) % 8) % 8;  // interior starts 16-byte aligned
+            P->storage_h.left_pad = lph;
+            P->storage_h.row_pitch = (lph + static_cast<uint64_t>(P->gx) + 7) / 8 * 8;
+            P->storage_h.plane_pitch = P->storage_h.row_pitch * static_cast<uint64_t>(P->gy);
+            P->storage_h.bytes = P->storage_h.plane_pitch * static_cast<uint64_t>(P->gz) * 2;
+            P->load_x0_h = static_cast<int>(lph & ~uint64_t{7});
+            stensor::BatchGeometry gh = geo;
+            gh.elem_bytes = 2;
+            gh.x_shift = static_cast<int>(lph & 7);
+            gh.patch_w = static_cast<int>(
+                sst::align_up(static_cast<uint32_t>(gh.x_shift + d->window_w + sst::kTileW * (gh.tiles_x - 1)), 8));
+            const int nks = static_cast<int>(P->img.a_smem.size() * 2 / 4096);
+            const auto& G = P->img.geo;
+            const int cps = P->variant->ctas_per_sm;
+            for (const auto& T : P->variant->h16c) {  // deepest pipeline that fits
+                const uint32_t tneed = sst::tmem_budget(static_cast<uint32_t>(T.nacc * sst::kTXB * P->variant->tyb),
+                                                        static_cast<uint32_t>(nks), true).need;
+                const int tcols = tneed <= 32 ? 32 : tneed <= 64 ? 64 : tneed <= 128 ? 128 : tneed <= 256 ? 256 : 512;
+                if (tneed > 512u / static_cast<uint32_t>(cps)) continue;
+                // occupancy guard as for the plan's own kernels (TMEM-blocked CTAs)
+                const int occ = std::min(max_smem, smem_per_sm / (std::max(cps, 512 / tcols) + 1));
+                const int s32 = std::max(occ, T.smem(false, nks, G.k_pad, G.patch_w, G.patch_h, G.patch_planes));
+                const int s16 = std::max(occ, T.smem(true, nks, G.k_pad, gh.patch_w, G.patch_h, G.patch_planes));
+                const int worst = std::max(s32, s16);
+                if (worst <= max_smem && (cps == 1 || cps * (worst + 1024) <= smem_per_sm)) {
+                    P->h16 = T;
+                    P->smem_f32_h = s32;
+                    P->smem_h = s16;
+                    P->tmem_cols_h = tcols;
+                    break;
+                }
+            }
+            if (gh.patch_w <= 256 && P->h16.launch) {
+                P->img_h = stensor::build_device_image(gh, d->rows, d->cols, d->a_values, d->a_meta, origin.data(),
+                                                       d->window_w, d->window_h);
+                ck(cudaMalloc(&P->d_gsrc_h, P->img_h.gather_src.size() * 4), "cudaMalloc");
+                ck(cudaMemcpy(P->d_gsrc_h, P->img_h.gather_src.data(), P->img_h.gather_src.size() * 4,
+                              cudaMemcpyHostToDevice), "cudaMemcpy");
+                ck(cudaMalloc(&P->d_gdst_h, P->img_h.gather_dst.size() * 4), "cudaMalloc");
+                ck(cudaMemcpy(P->d_gdst_h, P->img_h.gather_dst.data(), P->img_h.gather_dst.size() * 4,
+                              cudaMemcpyHostToDevice), "cudaMemcpy");
+                P->h16.configure(P->smem_f32_h, P->smem_h);
+                P->h16_ok = true;
+            }
+        }
         ck(cudaMalloc(&P->d_a, P->img.a_smem.size() * 2), "cudaMalloc");
         ck(cudaMemcpy(P->d_a, P->img.a_smem.data(), P->img.a_smem.size() * 2, cudaMemcpyHostToDevice),
            "cudaMemcpy");
@@ -824,6 +973,9 @@ sst_status sst_plan_stats_get(const sst_plan* plan, sst_plan_stats* s) {
         s->batches = p.nbatch;
         s->ctas = plan->grid_size(p);
         s->launches = plan->launches;
+        s->h16_launches = plan->h16_launches;
+        s->h16_capable = plan->h16_ok ? 1 : 0;
+        s->h16_patch_stages = plan->h16_ok ? plan->h16.np_h16 * 100 + plan->h16.nbb * 10 + plan->h16.nacc : 0;
         return SST_OK;
     } catch (...) {
         return sstc::from_current_exception();
@@ -860,6 +1012,8 @@ sst_status sst_plan_bind(sst_plan* plan, void* b0, void* b1) {
         ck(cudaMemset(plan->buf[0], 0, plan->storage.bytes), "cudaMemset");
         ck(cudaMemset(plan->buf[1], 0, plan->storage.bytes), "cudaMemset");
         plan->make_tmaps();
+        // binary16 storage pair up front (not inside the first timed run)
+        if (plan->h16_ok) plan->ensure_h16();
         return SST_OK;
     } catch (...) {
         return sstc::from_current_exception();

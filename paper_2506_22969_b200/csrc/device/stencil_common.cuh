@@ -172,8 +172,9 @@ __device__ __forceinline__ void store_a_tmem(const StepParams& p, const uint8_t*
     ptx::tmem_wait_st();
 }
 
-// Patch byte offsets of the 8 tile origins of each 8-tile group a gather warp owns.
-template <int TYB, int GPW>
+// Patch byte offsets of the 8 tile origins of each 8-tile group a gather warp owns
+// (ELEM: patch element bytes, 4 = fp32 storage, 2 = binary16 inter-step storage).
+template <int TYB, int GPW, int ELEM = 4>
 __device__ __forceinline__ void tile_offsets(int gw, int patch_w, int32_t (&toff)[GPW][8]) {
 #pragma unroll
     for (int gi = 0; gi < GPW; ++gi)
@@ -181,7 +182,7 @@ __device__ __forceinline__ void tile_offsets(int gw, int patch_w, int32_t (&toff
         for (int t = 0; t < 8; ++t) {
             int tx, ty;
             tile_of_column<TYB>((gw + kGatherWarps * gi) * 8 + t, tx, ty);
-            toff[gi][t] = (ty * kTileH * patch_w + tx * kTileW) * 4;
+            toff[gi][t] = (ty * kTileH * patch_w + tx * kTileW) * ELEM;
         }
 }
 
@@ -191,7 +192,10 @@ __device__ __forceinline__ void tile_offsets(int gw, int patch_w, int32_t (&toff
 // conversion, so the loop is not bound by one LDS round trip per sweep.
 // LO: the sweep writes the low term of the split operand, f16(v - f16(v)) (exact
 // residual in f32; B_hi + B_lo carries ~22 significant bits of v).
-template <int GPW, int UNR, bool LO = false>
+// HIN: the patch holds binary16 storage (the previous step's outputs already rounded
+// to binary16 RNE by its epilogue, i.e. exactly the value the f32 path's conversion
+// here would produce): the gather copies the bits.
+template <int GPW, int UNR, bool LO = false, bool HIN = false>
 __device__ __forceinline__ void gather_sweeps(uint32_t pbase, uint32_t bbase, const int32_t* sGsrc,
                                               const int32_t* sGdst, int j0, int gw, uint32_t gstride,
                                               uint32_t lane, const int32_t (&toff)[GPW][8]) {
@@ -200,6 +204,30 @@ __device__ __forceinline__ void gather_sweeps(uint32_t pbase, uint32_t bbase, co
     for (int u = 0; u < UNR; ++u) {
         src[u] = pbase + static_cast<uint32_t>(sGsrc[(j0 + u) * 32 + lane]);
         dst[u] = bbase + static_cast<uint32_t>(sGdst[(j0 + u) * 32 + lane]);
+    }
+    if constexpr (HIN) {
+        static_assert(!LO, "split operands need fp32 storage");
+        uint32_t hv[UNR][GPW][8];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+            for (int gi = 0; gi < GPW; ++gi)
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(hv[u][gi][t]) : "r"(src[u] + toff[gi][t]));
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+            for (int gi = 0; gi < GPW; ++gi) {
+                uint32_t h[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) h[i] = __byte_perm(hv[u][gi][2 * i], hv[u][gi][2 * i + 1], 0x5410);
+                const uint32_t d = dst[u] + static_cast<uint32_t>(gw + kGatherWarps * gi) * gstride;
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(d), "r"(h[0]), "r"(h[1]), "r"(h[2]),
+                             "r"(h[3])
+                             : "memory");
+            }
+        return;
     }
     float v[UNR][GPW][8];
 #pragma unroll
@@ -231,24 +259,28 @@ __device__ __forceinline__ void gather_sweeps(uint32_t pbase, uint32_t bbase, co
         }
 }
 
-template <int GPW, bool LO>
+template <int GPW, bool LO, bool HIN = false>
 __device__ __forceinline__ void gather_range(uint32_t pbase, uint32_t bbase, const int32_t* sGsrc,
                                              const int32_t* sGdst, int j, int j_end, int gw, uint32_t gstride,
                                              uint32_t lane, const int32_t (&toff)[GPW][8]) {
     constexpr int UNR = GPW >= 2 ? 2 : 3;  // 24-32 loads in flight per lane
 #pragma unroll 1
     for (; j + UNR <= j_end; j += UNR)
-        gather_sweeps<GPW, UNR, LO>(pbase, bbase, sGsrc, sGdst, j, gw, gstride, lane, toff);
+        gather_sweeps<GPW, UNR, LO, HIN>(pbase, bbase, sGsrc, sGdst, j, gw, gstride, lane, toff);
 #pragma unroll 1
-    for (; j < j_end; ++j) gather_sweeps<GPW, 1, LO>(pbase, bbase, sGsrc, sGdst, j, gw, gstride, lane, toff);
+    for (; j < j_end; ++j) gather_sweeps<GPW, 1, LO, HIN>(pbase, bbase, sGsrc, sGdst, j, gw, gstride, lane, toff);
 }
 
 // Sweeps [0, lo0) write B'' (or B_hi), sweeps [lo0, nsweeps) B_lo (SST_PREC_F16X2).
-template <int GPW>
+template <int GPW, bool HIN = false>
 __device__ __forceinline__ void gather_batch(uint32_t pbase, uint32_t bbase, const int32_t* sGsrc,
                                              const int32_t* sGdst, int nsweeps, int gw,
                                              uint32_t gstride, uint32_t lane,
                                              const int32_t (&toff)[GPW][8], int lo0) {
+    if constexpr (HIN) {  // binary16 storage: f16 operands only (no split)
+        gather_range<GPW, false, true>(pbase, bbase, sGsrc, sGdst, 0, nsweeps, gw, gstride, lane, toff);
+        return;
+    }
     const int hi_end = min(nsweeps, lo0);
     gather_range<GPW, false>(pbase, bbase, sGsrc, sGdst, 0, hi_end, gw, gstride, lane, toff);
     if (hi_end < nsweeps)
@@ -471,6 +503,90 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
                 else
                     tma_store_3d(peer_down, sS + buf + c * s_stride, bx0, Y0, Z0 - p.peer_down_c0);
             }
+        }
+        bulk_commit();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// binary16 inter-step storage (SST_PREC_F16, steps 1 .. T-1 of a run): the epilogue
+// rounds the f32 accumulator to binary16 RNE — the value every consumer (the next
+// step's gather) would compute from the f32 store — and stores 2 B per update.
+// A batch (128 x 8*TYB outputs) stages as two 64-half (128 B) SWIZZLE_128B boxes.
+// TMA clips stores in 16-byte units (8 halves): the store map ends at ox8 = ox & ~7
+// and the <= 7 columns [ox8, ox) are plain 2-byte stores.
+template <int DIMS, int TYB>
+__device__ __forceinline__ void store_right_edge_h(const StepParams& p, __half* dst,
+                                                   const uint32_t (&v)[kTXB / 2][2 * TYB], int X0, int Y0,
+                                                   int Z0, uint32_t q, uint32_t lane) {
+    constexpr int NBOX = kTXB / 2;
+    const int ox = p.gx - 2 * p.r, ox8 = ox & ~7;
+    if (X0 + kTXB * kTileW <= ox8 || (p.debug_mode & 8)) return;
+    const int dxl = static_cast<int>(q) * 4 + static_cast<int>(lane / 8);
+    const int y_lim = DIMS == 2 ? p.slow_hi : p.y_end;
+    const int y0 = Y0 + static_cast<int>(lane % 8);
+    __half* rowp = dst + (DIMS == 3 ? static_cast<int64_t>(Z0 + p.r) * p.plane_pitch : 0) +
+                   static_cast<int64_t>(y0 + p.r) * p.row_pitch + p.left_pad + p.r + X0 + dxl;
+    const int64_t ystep = static_cast<int64_t>(kTileH) * p.row_pitch;
+#pragma unroll
+    for (int c = 0; c < NBOX; ++c)
+#pragma unroll
+        for (int par = 0; par < 2; ++par) {
+            const int xo = c * kBoxW + par * kTileW;
+            const int xr = X0 + xo + dxl;
+            if (xr >= ox8 && xr < ox) {
+#pragma unroll
+                for (int ty = 0; ty < TYB; ++ty)
+                    if (y0 + ty * kTileH < y_lim)
+                        rowp[xo + ty * ystep] = __float2half_rn(__uint_as_float(v[c][2 * ty + par]));
+            }
+        }
+}
+
+template <int DIMS, int TYB, int NS>
+__device__ __forceinline__ void store_batch_h(const StepParams& p, const CUtensorMap* tmap_out, __half* dst,
+                                              const uint32_t (&v)[kTXB / 2][2 * TYB], uint8_t* sS,
+                                              uint32_t s_stride, int nb, int X0, int Y0, int Z0, uint32_t q,
+                                              uint32_t lane, int etid) {
+    using namespace ptx;
+    constexpr int CW = 2 * TYB, NBOX = kTXB / 2;
+    constexpr int HBOX = 64;  // halves per 128-byte box row
+    const uint32_t dy = lane % 8;
+    const uint32_t inchunk = ((q & 1u) * 4u + lane / 8u) * 2u;  // byte of dx % 8 inside its 16 B chunk
+    const int ox = p.gx - 2 * p.r, ox8 = ox & ~7;
+    store_right_edge_h<DIMS, TYB>(p, dst, v, X0, Y0, Z0, q, lane);
+    // a binary16 batch fills half an fp32 staging slot: 2 NS buffers, so the TMA
+    // stores of batch n read one while batch n + 1 stages into the next
+    constexpr int NSH = 2 * NS;
+    const uint32_t buf = static_cast<uint32_t>(nb % NSH) * (NBOX / 2) * s_stride;
+    const uint32_t stage = smem_u32(sS) + buf;
+    if (etid == 0) bulk_wait_read<NSH - 1>();
+    named_bar_sync(kEpiBarrier, kEpiWarps * 32);
+#pragma unroll
+    for (int c = 0; c < NBOX; ++c)
+#pragma unroll
+        for (int i = 0; i < CW; ++i) {
+            // x in the batch = 32c + 16 (i & 1) + dx, dx = 4q + lane / 8; box c / 2 holds
+            // x in [64 (c / 2), 64 (c / 2) + 64): 16-byte chunk 4 (c & 1) + 2 (i & 1) + q / 2
+            const uint32_t y = static_cast<uint32_t>(i / 2) * kTileH + dy;
+            const uint32_t chunk = (static_cast<uint32_t>(c & 1) * 4u + static_cast<uint32_t>(i & 1) * 2u + q / 2u) ^ dy;
+            const __half h = __float2half_rn(__uint_as_float(v[c][i]));
+            asm volatile("st.shared.b16 [%0], %1;" ::"r"(stage + static_cast<uint32_t>(c / 2) * s_stride + y * 128u +
+                                                         chunk * 16u + inchunk),
+                         "h"(*reinterpret_cast<const unsigned short*>(&h))
+                         : "memory");
+        }
+    named_bar_sync(kEpiBarrier, kEpiWarps * 32);
+    if (etid == 0 && !(p.debug_mode & 64)) {
+        fence_proxy_async_smem();
+#pragma unroll
+        for (int cb = 0; cb < NBOX / 2; ++cb) {
+            const int bx0 = X0 + cb * HBOX;
+            if (bx0 >= ox8) break;  // fully clipped
+            if (DIMS == 2)
+                tma_store_2d(tmap_out, sS + buf + cb * s_stride, bx0, Y0 - p.slow_lo);
+            else
+                tma_store_3d(tmap_out, sS + buf + cb * s_stride, bx0, Y0, Z0);
         }
         bulk_commit();
     }

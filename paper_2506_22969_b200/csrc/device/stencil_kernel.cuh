@@ -36,7 +36,8 @@ __host__ __device__ inline uint32_t align_up(uint32_t v, uint32_t a) { return (v
 template <int TYB>
 __host__ __device__ inline SmemLayout smem_layout_generic(int nks, int k_pad, int patch_w, int patch_h,
                                                           int planes, int np, int nbb, int nbars,
-                                                          int ns = kStageBufs, bool a_in_tmem = false) {
+                                                          int ns = kStageBufs, bool a_in_tmem = false,
+                                                          int elem = 4) {
     constexpr int N = kTXB * TYB;
     SmemLayout L{};
     uint32_t o = 0;
@@ -48,7 +49,7 @@ __host__ __device__ inline SmemLayout smem_layout_generic(int nks, int k_pad, in
     L.s_stride = align_up(static_cast<uint32_t>(kBoxW * kTileH * TYB) * 4u, 1024);
     L.s = o = align_up(o, 1024);
     o += ns * (kTXB / 2) * L.s_stride;
-    L.p_stride = align_up(static_cast<uint32_t>(patch_w * patch_h * planes) * 4u, 128);
+    L.p_stride = align_up(static_cast<uint32_t>(patch_w * patch_h * planes * elem), 128);
     L.p = o = align_up(o, 128);
     o += np * L.p_stride;
     // the prologue stages the A'' image / metadata words in [L.b, L.gsrc) before
@@ -75,17 +76,18 @@ __host__ __device__ inline SmemLayout smem_layout_generic(int nks, int k_pad, in
 // kBidSlots iterations ahead of the epilogue through the patch / B'' / accumulator
 // rings, 3 + 2 + 2 deep).
 constexpr int kBidSlots = 16;
+constexpr int kDrawAhead = 2;  // dynamic scheduling: counter draws in flight per CTA
 // dynamic multi-step mode: items committed but not yet published (publication every
 // kPubEvery items, lagging kPubLag store groups)
 constexpr int kPubEvery = 8, kPubLag = 2, kPubRing = 16;
 static_assert(kPubRing >= kPubEvery + kPubLag + 1, "publication ring");
 
-template <int TYB, int NP, bool AT, int NS = kStageBufs>
+template <int TYB, int NP, bool AT, int NS = kStageBufs, int NBB = 2, int NACC = 2>
 __host__ __device__ inline SmemLayout smem_layout(int nks, int k_pad, int patch_w, int patch_h,
-                                                  int planes) {
-    static_assert(kBidSlots > NP + 4, "batch-index ring vs pipeline depth");
-    SmemLayout L = smem_layout_generic<TYB>(nks, k_pad, patch_w, patch_h, planes, NP, 2, 2 * NP + 8 + kBidSlots,
-                                            NS, AT);
+                                                  int planes, int elem = 4) {
+    static_assert(kBidSlots > NP + NBB + NACC, "batch-index ring vs pipeline depth");
+    SmemLayout L = smem_layout_generic<TYB>(nks, k_pad, patch_w, patch_h, planes, NP, NBB,
+                                            2 * NP + 2 * NBB + 2 * NACC + kBidSlots, NS, AT, elem);
     L.ring = align_up(L.total, 16);  // the batch-index ring (int32 x kBidSlots), then the
                                      // dynamic multi-step mode's unpublished items (kPubRing)
     L.total = align_up(L.ring + (kBidSlots + kPubRing) * 4, 128);
@@ -146,7 +148,13 @@ enum StepMode { kModeStatic = 0, kModeDynamic = 1, kModeMulti = 2, kModePeer = 3
 // into the next; 1 = the epilogue waits for each batch's stores to leave smem)
 // CPS: CTAs per SM the variant is built for (2: small-smem variants whose two co-resident
 // CTAs overlap one another's pipeline bubbles; registers capped accordingly)
-template <int DIMS, int TYB, int NP, bool AT, int MODE = kModeStatic, int NS = kStageBufs, int CPS = 1>
+// HIN / HOUT: the input / output grid is binary16 storage (SST_PREC_F16 runs keep
+// steps 1 .. T-1 in binary16: bitwise the same result, half the bytes per update);
+// the out map and p's pitches / left pad then describe the f16 buffer, the in map,
+// gather tables and patch width the input's storage.
+// NBB / NACC: B'' operand stages in smem / accumulator stages in TMEM.
+template <int DIMS, int TYB, int NP, bool AT, int MODE = kModeStatic, int NS = kStageBufs, int CPS = 1,
+          bool HIN = false, bool HOUT = false, int NBB = 2, int NACC = 2>
 __global__ void __launch_bounds__(kThreads, CPS)
     stencil_step_kernel(const __grid_constant__ MapSet maps, const StepParams p) {
     constexpr int N = kTXB * TYB;
@@ -160,7 +168,9 @@ __global__ void __launch_bounds__(kThreads, CPS)
     using namespace ptx;
 
     extern __shared__ __align__(1024) uint8_t smem[];
-    const SmemLayout L = smem_layout<TYB, NP, AT, NS>(p.nks, p.k_pad, p.patch_w, p.patch_h, p.patch_planes);
+    constexpr int ELEM = HIN ? 2 : 4;  // patch element bytes
+    const SmemLayout L =
+        smem_layout<TYB, NP, AT, NS, NBB, NACC>(p.nks, p.k_pad, p.patch_w, p.patch_h, p.patch_planes, ELEM);
     uint8_t* sA = smem + L.a;
     uint8_t* sB = smem + L.b;  // 2 stages
     uint8_t* sS = smem + L.s;  // output staging
@@ -171,10 +181,10 @@ __global__ void __launch_bounds__(kThreads, CPS)
     uint64_t* patch_full = bars;
     uint64_t* patch_empty = bars + NP;
     uint64_t* b_full = bars + 2 * NP;
-    uint64_t* b_empty = b_full + 2;
-    uint64_t* d_full = b_full + 4;
-    uint64_t* d_empty = b_full + 6;
-    uint64_t* bid_full = b_full + 8;  // [kBidSlots]
+    uint64_t* b_empty = b_full + NBB;
+    uint64_t* d_full = b_empty + NBB;
+    uint64_t* d_empty = d_full + NACC;
+    uint64_t* bid_full = d_empty + NACC;  // [kBidSlots]
     int32_t* sBid = reinterpret_cast<int32_t*>(smem + L.ring);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem_slot);
 
@@ -187,9 +197,11 @@ __global__ void __launch_bounds__(kThreads, CPS)
             mbar_init(&patch_full[s], 1);
             mbar_init(&patch_empty[s], kGatherWarps);
         }
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < NBB; ++s) {
             mbar_init(&b_full[s], kGatherWarps);
             mbar_init(&b_empty[s], 1);
+        }
+        for (int s = 0; s < NACC; ++s) {
             mbar_init(&d_full[s], 1);
             mbar_init(&d_empty[s], kEpiWarps);
         }
@@ -213,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
     mbar_wait(pbar, 0);  // constants in smem
     const uint32_t tmem = *tmem_slot;
     // TMEM: two accumulators, the metadata columns, then (AT) the A'' operand
-    const TmemCols tc = tmem_budget(2 * N, static_cast<uint32_t>(p.nks), AT);
+    const TmemCols tc = tmem_budget(NACC * N, static_cast<uint32_t>(p.nks), AT);
     const uint32_t e_col = tc.e_col;
     if (warp >= kEpiWarp0) {
         store_metadata<AT>(p, sB, tmem, e_col, static_cast<uint32_t>(warp % 4), lane);
@@ -265,24 +277,30 @@ __global__ void __launch_bounds__(kThreads, CPS)
     } else if (warp == 0) {
         // ------------------------------------------------------ TMA producer
         // (the whole warp walks the loop: lane 0 issues, all lanes refresh counters)
-        const uint32_t pbytes = static_cast<uint32_t>(p.patch_w * p.patch_h * p.patch_planes) * 4u;
+        const uint32_t pbytes = static_cast<uint32_t>(p.patch_w * p.patch_h * p.patch_planes * ELEM);
         uint32_t polls = 0, known = p.flag_base;  // min over all progress counters seen
         int r = 0;                                // real (non no-op) iterations
         if constexpr (dyn) {
-            // a CTA's first batch is blockIdx.x, later ones G + counter draws; the
-            // next index is drawn one batch ahead so the atomic's latency hides
-            // behind the current batch's wait / issue
-            uint32_t nxt = blockIdx.x;
-            for (;; ++r) {
+            // a CTA's first batch is blockIdx.x, later ones G + counter draws. Draws
+            // run kDrawAhead batches ahead in a FIFO of registers (two slots, the loop
+            // unrolled over them): the atomic's round trip (~0.7 us under load) would
+            // otherwise bound the producer to one batch per round trip (binary16
+            // patches: loads-only ablation 3.3 TB/s). Consuming slots in draw order
+            // keeps the counter exact: each consumed batch triggers one draw, so a
+            // launch advances it by nitems + G * (kDrawAhead - 1), and the first
+            // invalid slot a CTA meets is followed only by invalid ones.
+            uint32_t q0 = blockIdx.x, q1 = 0;
+            if (lane == 0) q1 = static_cast<uint32_t>(G) + atomicAdd(p.sched, 1u) - p.sched_base;
+            auto item = [&](uint32_t& slot) -> bool {
                 int g = -1;
                 if (lane == 0) {
-                    g = nxt < static_cast<uint32_t>(nitems) ? static_cast<int>(nxt) : -1;
-                    if (g >= 0) nxt = static_cast<uint32_t>(G) + atomicAdd(p.sched, 1u) - p.sched_base;
+                    g = slot < static_cast<uint32_t>(nitems) ? static_cast<int>(slot) : -1;
+                    if (g >= 0) slot = static_cast<uint32_t>(G) + atomicAdd(p.sched, 1u) - p.sched_base;
                     sBid[r % kBidSlots] = g;
                     mbar_arrive(&bid_full[r % kBidSlots]);
                 }
                 g = __shfl_sync(0xffffffffu, g, 0);
-                if (g < 0) break;
+                if (g < 0) return false;
                 const int t = mdyn ? g / p.nbatch : 0, b = mdyn ? g - t * p.nbatch : g;
                 int X0, Y0, Z0;
                 batch_coords(b, X0, Y0, Z0);
@@ -314,6 +332,10 @@ __global__ void __launch_bounds__(kThreads, CPS)
                         tma_load_3d(dst, tin, &patch_full[s], X0 + p.load_x0, Y0, Z0);
                 }
                 __syncwarp();
+                ++r;
+                return true;
+            };
+            while (item(q0) && item(q1)) {
             }
         }
         for (int j = 0; j < (dyn ? 0 : total); ++j) {
@@ -366,10 +388,9 @@ __global__ void __launch_bounds__(kThreads, CPS)
                     continue;
                 }
             }
-            const int s = r & 1;
-            const uint32_t ph = (r >> 1) & 1;
-            mbar_wait(&b_full[s], ph);
-            mbar_wait(&d_empty[s], ph ^ 1);
+            const int s = r % NBB, sa = r % NACC;
+            mbar_wait(&b_full[s], (r / NBB) & 1);
+            mbar_wait(&d_empty[sa], ((r / NACC) & 1) ^ 1);
             tc_fence_after();
             if (elect_one()) {
                 const uint32_t b0 = smem_u32(sB + s * L.b_stride);
@@ -378,16 +399,16 @@ __global__ void __launch_bounds__(kThreads, CPS)
                     const uint64_t bd = make_smem_desc(b0 + ks * 512u, 128, b_sbo);
                     const uint32_t ea = tmem + e_col + static_cast<uint32_t>(ks);
                     if constexpr (AT) {
-                        mma_sp_f16_ts(tmem + static_cast<uint32_t>(s * N), tmem + tc.a_col + ks * 8u, bd,
+                        mma_sp_f16_ts(tmem + static_cast<uint32_t>(sa * N), tmem + tc.a_col + ks * 8u, bd,
                                       ea & ~1u, idesc | (ea & 1u), ks > 0 ? 1u : 0u);
                     } else {
                         const uint64_t ad = make_smem_desc(a0 + ks * 4096u, 128, 256);
-                        mma_sp_f16(tmem + static_cast<uint32_t>(s * N), ad, bd, ea & ~1u,
+                        mma_sp_f16(tmem + static_cast<uint32_t>(sa * N), ad, bd, ea & ~1u,
                                    idesc | (ea & 1u), ks > 0 ? 1u : 0u);
                     }
                 }
                 mma_commit(&b_empty[s]);
-                mma_commit(&d_full[s]);
+                mma_commit(&d_full[sa]);
             }
             __syncwarp();
         }
@@ -396,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
         const int gw = warp - kGatherWarp0;
         const bool active = gw < NGROUP;
         int32_t toff[GPW][8];
-        tile_offsets<TYB, GPW>(gw, p.patch_w, toff);
+        tile_offsets<TYB, GPW, ELEM>(gw, p.patch_w, toff);
         const uint32_t gstride = static_cast<uint32_t>(p.k_pad) * 16u;  // bytes per 8-tile group
         const int nsweeps = (active && !(p.debug_mode & 2)) ? p.k_pad / 32 : 0;
         int r = 0;
@@ -413,11 +434,10 @@ __global__ void __launch_bounds__(kThreads, CPS)
             }
             const int ps = r % NP;
             const uint32_t pph = (r / NP) & 1;
-            const int s = r & 1;
-            const uint32_t ph = (r >> 1) & 1;
+            const int s = r % NBB;
             mbar_wait(&patch_full[ps], pph);
-            mbar_wait(&b_empty[s], ph ^ 1);
-            gather_batch<GPW>(smem_u32(sP + ps * L.p_stride), smem_u32(sB + s * L.b_stride), sGsrc,
+            mbar_wait(&b_empty[s], ((r / NBB) & 1) ^ 1);
+            gather_batch<GPW, HIN>(smem_u32(sP + ps * L.p_stride), smem_u32(sB + s * L.b_stride), sGsrc,
                               sGdst, nsweeps, gw, gstride, lane, toff, p.lo_sweep0);
             fence_proxy_async_smem();  // generic-proxy writes -> tensor-core reads
             __syncwarp();
@@ -473,8 +493,8 @@ __global__ void __launch_bounds__(kThreads, CPS)
                 }
             }
             batch_coords(b, X0, Y0, Z0);
-            const int s = r & 1;
-            const uint32_t ph = (r >> 1) & 1;
+            const int s = r % NACC;
+            const uint32_t ph = (r / NACC) & 1;
             ++r;
             uint32_t v[NBOX][CW];
             if (p.debug_mode & 32) {  // store-only ablation
@@ -503,9 +523,14 @@ __global__ void __launch_bounds__(kThreads, CPS)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&d_empty[s]);
             }
-            if constexpr (DIMS == 2)
+            if constexpr (DIMS == 2 && !HOUT)
                 if (p.fold_ring != nullptr) fold_keep_ring<TYB>(p, v, X0, Y0, q, lane);
-            if (!(p.debug_mode & 1))
+            if constexpr (HOUT) {
+                if (!(p.debug_mode & 1))
+                    store_batch_h<DIMS, TYB, NS>(p, &maps.out[(p.src + t + 1) & 1],
+                                                 reinterpret_cast<__half*>(buf_of(p, (p.src + t + 1) & 1)), v, sS,
+                                                 L.s_stride, r - 1, X0, Y0, Z0, q, lane, etid);
+            } else if (!(p.debug_mode & 1))
             {
                 const int par = (p.src + t + 1) & 1;
                 store_batch<DIMS, TYB, NS, kEdgePlain, peer>(

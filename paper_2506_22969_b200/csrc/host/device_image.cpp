@@ -56,10 +56,12 @@ double f16_bits_to_double(std::uint16_t h) {
 
 namespace {
 
-// distinct addresses per bank among the 32 lanes of one gather LDS
-int bank_degree(const std::array<std::int32_t, 32>& addr) {
+// distinct 4-byte words per bank among the 32 lanes of one gather LDS (addresses
+// in patch elements of `elem` bytes: two binary16 lanes may share a word)
+int bank_degree(const std::array<std::int32_t, 32>& addr, int elem) {
     std::array<std::vector<std::int32_t>, 32> per_bank;
-    for (std::int32_t a : addr) {
+    for (std::int32_t e : addr) {
+        const std::int32_t a = e * elem / 4;
         auto& v = per_bank[static_cast<std::size_t>(((a % 32) + 32) % 32)];
         if (std::find(v.begin(), v.end(), a) == v.end()) v.push_back(a);
     }
@@ -68,7 +70,7 @@ int bank_degree(const std::array<std::int32_t, 32>& addr) {
     return static_cast<int>(worst);
 }
 
-int schedule_cost(const std::vector<std::uint8_t>& order, const std::vector<std::int32_t>& koff,
+int schedule_cost(const std::vector<std::uint8_t>& order, const std::vector<std::int32_t>& koff, int elem,
                   int* worst_out) {
     int total = 0, worst = 0;
     for (std::size_t it = 0; it * 4 < order.size(); ++it) {
@@ -77,7 +79,7 @@ int schedule_cost(const std::vector<std::uint8_t>& order, const std::vector<std:
             addr[static_cast<std::size_t>(lane)] =
                 koff[static_cast<std::size_t>(order[it * 4 + static_cast<std::size_t>(lane / 8)]) * 8 +
                      static_cast<std::size_t>(lane % 8)];
-        const int d = bank_degree(addr);
+        const int d = bank_degree(addr, elem);
         total += d;
         worst = std::max(worst, d);
     }
@@ -162,19 +164,19 @@ DeviceImage build_device_image(const BatchGeometry& geo_in, std::size_t rows, st
     const std::size_t ngroups = k_pad / 8;
     img.kgroup_order.resize(ngroups);
     std::iota(img.kgroup_order.begin(), img.kgroup_order.end(), std::uint8_t{0});
-    int best = schedule_cost(img.kgroup_order, img.koff, nullptr);
+    int best = schedule_cost(img.kgroup_order, img.koff, g.elem_bytes, nullptr);
     std::mt19937 rng(12345);
     for (int trial = 0; trial < 4000 && ngroups > 4; ++trial) {
         const std::size_t a = rng() % ngroups, b = rng() % ngroups;
         if (a / 4 == b / 4) continue;
         std::swap(img.kgroup_order[a], img.kgroup_order[b]);
-        const int c = schedule_cost(img.kgroup_order, img.koff, nullptr);
+        const int c = schedule_cost(img.kgroup_order, img.koff, g.elem_bytes, nullptr);
         if (c <= best)
             best = c;
         else
             std::swap(img.kgroup_order[a], img.kgroup_order[b]);
     }
-    schedule_cost(img.kgroup_order, img.koff, &img.worst_bank_conflict);
+    schedule_cost(img.kgroup_order, img.koff, g.elem_bytes, &img.worst_bank_conflict);
 
     // ---- per-lane gather tables: sweep j, lane -> (patch byte offset, B byte offset)
     img.gather_src.resize(k_pad / 32 * 32);
@@ -182,7 +184,7 @@ DeviceImage build_device_image(const BatchGeometry& geo_in, std::size_t rows, st
     for (std::size_t j = 0; j < k_pad / 32; ++j)
         for (std::size_t lane = 0; lane < 32; ++lane) {
             const std::size_t k = static_cast<std::size_t>(img.kgroup_order[4 * j + lane / 8]) * 8 + lane % 8;
-            img.gather_src[j * 32 + lane] = img.koff[k] * 4;
+            img.gather_src[j * 32 + lane] = img.koff[k] * g.elem_bytes;
             img.gather_dst[j * 32 + lane] = static_cast<std::int32_t>(k) * 16;
         }
     img.lo_sweep0 = static_cast<int>(k_pad / 32);

@@ -25,6 +25,7 @@ struct BatchGeometry {
     int terms = 1;             // 2: split B'' = B_hi + B_lo (SST_PREC_F16X2); K doubled
     int x_shift = 0;           // patch column of the window origin (TMA boxes start
                                // 16-byte aligned, so the patch begins lp cells early)
+    int elem_bytes = 4;        // patch element: 4 (fp32 storage) or 2 (binary16 inter-step storage)
     int n_tiles() const { return tiles_x * tiles_y; }
 };
 

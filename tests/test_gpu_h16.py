@@ -1,0 +1,110 @@
+"""Binary16 inter-step storage (SST_PREC_F16 runs of T >= 2 steps).
+
+Steps 1 .. T-1 are stored as binary16 (RNE in the producing epilogue) and the
+last step as fp32. The only consumer of an intermediate grid is the next step's
+gather, which rounds its operand to binary16 RNE (the reference round16
+semantics, fp16.hpp:13-59), so the result must be BITWISE the fp32-storage
+result — over the whole grid, boundary ring included. SST_H16=0 selects the
+fp32-storage path for the comparison (read per call).
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2506_22969_b200 import SparseStencil, valid_core
+
+pytestmark = pytest.mark.gpu
+
+
+def run_both(name, grid, steps, fuse=1):
+    eng = SparseStencil(name, list(grid.shape), fuse=fuse)
+    try:
+        assert eng.stats()["h16_capable"] == 1
+        os.environ["SST_H16"] = "0"
+        ref = eng.apply_host(grid, steps)
+        s0 = eng.stats()
+        os.environ["SST_H16"] = "1"
+        got = eng.apply_host(grid, steps)
+        s1 = eng.stats()
+    finally:
+        os.environ.pop("SST_H16", None)
+        eng.close()
+    launches = steps // fuse
+    assert s0["h16_launches"] == 0
+    assert s1["h16_launches"] == (launches if launches > 1 else 0)
+    assert s1["launches"] - s0["launches"] == launches
+    return ref, got, eng
+
+
+@pytest.mark.parametrize("name", ["Heat-2D", "Box-2D9P", "Star-2D13P", "Box-2D49P"])
+@pytest.mark.parametrize("dims", [(97, 301), (130, 129), (21, 23), (70, 10), (300, 517), (9, 9)])
+@pytest.mark.parametrize("steps", [2, 3, 6])
+def test_h16_storage_bitwise_equals_f32_storage(gpu, name, dims, steps):
+    g = oracle.random_grid(dims, seed=11).astype(np.float32)
+    ref, got, _ = run_both(name, g, steps)
+    assert np.array_equal(ref.view(np.uint32), got.view(np.uint32))
+
+
+@pytest.mark.parametrize("name,dims,steps", [("Heat-2D", (256, 384), 10), ("Box-2D9P", (333, 290), 25),
+                                             ("Star-2D13P", (300, 260), 8)])
+def test_h16_storage_matches_round16_oracle(gpu, name, dims, steps):
+    g = oracle.random_grid(dims, seed=3)
+    ref, got, eng = run_both(name, g.astype(np.float32), steps)
+    core = valid_core(got, steps, eng.r).astype(np.float64)
+    assert np.array_equal(core, oracle.direct_apply_mt(name, g, steps, round16=True))
+
+
+def test_h16_wide_range_values(gpu):
+    """Values outside binary16's normal range (overflow to inf, subnormals, signs):
+    the epilogue's RNE and the gather's RNE see the same f32 value."""
+    rng = np.random.default_rng(5)
+    g = (rng.standard_normal((200, 333)) * np.exp2(rng.integers(-30, 18, (200, 333)))).astype(np.float32)
+    ref, got, _ = run_both("Box-2D9P", g, 4)
+    assert np.array_equal(ref.view(np.uint32), got.view(np.uint32))
+
+
+def test_h16_fused_operator(gpu):
+    g = oracle.random_grid((257, 300), seed=12).astype(np.float32)
+    ref, got, _ = run_both("Box-2D9P", g, 8, fuse=2)
+    assert np.array_equal(ref.view(np.uint32), got.view(np.uint32))
+
+
+def test_h16_full_size_box2d(gpu):
+    """BASELINE configs[1] grid: 8192^2, 20 steps, whole grid bitwise."""
+    g = oracle.random_grid((8192, 8192), seed=1).astype(np.float32)
+    ref, got, _ = run_both("Box-2D9P", g, 20)
+    assert np.array_equal(ref.view(np.uint32), got.view(np.uint32))
+
+
+def test_h16_run_steps_device_buffers(gpu):
+    """sst_run_steps on device buffers: the result lands in the buffer plain
+    ping-pong ends on ((src + T) & 1), both parities, and the other buffer's
+    ring is untouched."""
+    import torch
+
+    g = oracle.random_grid((150, 260), seed=13).astype(np.float32)
+    want = {}
+    for h16 in ("0", "1"):
+        os.environ["SST_H16"] = h16
+        eng = SparseStencil("Star-2D13P", [150, 260])
+        try:
+            eng.bind()
+            for src in (0, 1):
+                for steps in (2, 5):
+                    eng.upload(torch.from_numpy(g).cuda(), src)
+                    torch.cuda.synchronize()
+                    dst = eng.run(steps, src)
+                    assert dst == (src + steps) & 1
+                    out = eng.download(dst)
+                    key = (src, steps)
+                    if h16 == "0":
+                        want[key] = out
+                    else:
+                        assert np.array_equal(out.view(np.uint32), want[key].view(np.uint32))
+        finally:
+            os.environ.pop("SST_H16", None)
+            eng.close()

@@ -64,5 +64,5 @@ for v in variants:
             cells *= d
         print(f"variant {v:2d} mode {m} : {us:8.2f} us/launch  {cells * fuse / us / 1e3:7.1f} GSt/s  "
               f"patch {st['patch_w']}x{st['patch_h']}x{st['patch_planes']} stages {st['patch_stages']} "
-              f"ctas {st['ctas']} smem {st['smem_bytes']}", flush=True)
+              f"ctas {st['ctas']} smem {st['smem_bytes']} h16 {st['h16_patch_stages']}", flush=True)
         eng.close()
