@@ -23,6 +23,8 @@
  *                          with ping-pong buffers; replaces the step loop of
  *                          direct_apply (stencil.hpp:72, stencil.cpp:239-268)
  *   sst_apply_host         direct_apply(spec, grid, steps) end to end from host memory
+ *   sst_run_steps_multi    the same sweep slab-decomposed over the GPUs of a node (no
+ *                          reference counterpart: the reference is single-threaded)
  *   sst_run_compile        run_compile(CompileRequest) (pipeline.hpp:14-46, pipeline.cpp:52-198):
  *                          report.json / a2.s24 / lut.bin, desk-scale verification on the GPU
  *   sst_explore            explore_layouts (perf.hpp:45-51), the CLI's `explore` table
@@ -210,6 +212,42 @@ SST_API sst_status sst_ipc_close(void* dev_ptr);
 /* Stream-ordered flag write / wait (cuStreamWriteValue32 / cuStreamWaitValue32 GEQ). */
 SST_API sst_status sst_stream_write_u32(void* stream, uint32_t* dev_addr, uint32_t value);
 SST_API sst_status sst_stream_wait_geq_u32(void* stream, uint32_t* dev_addr, uint32_t value);
+
+/* The per-step P2P schedule of one slab in C (what a rank of a multi-process run
+ * calls instead of looping over sst_stream_wait_geq_u32 / sst_run_steps /
+ * sst_stream_write_u32 itself): for launch u = launch0, launch0 + 1, ... wait until
+ * my_flags[0] >= u (upper neighbour, if any) and my_flags[1] >= u (lower one), run one
+ * operator application, then write u + 1 into *up_flag / *down_flag (the neighbours'
+ * flag words naming this slab: the upper's [1], the lower's [0]). */
+SST_API sst_status sst_run_steps_peer(sst_plan* plan, int src, uint64_t steps, void* stream, uint32_t* my_flags,
+                                      uint32_t* up_flag, uint32_t* down_flag, uint32_t launch0, int* dst_out);
+/* Slices [first, first + count) of the slowest axis of buffer `which` -> dense dst. */
+SST_API sst_status sst_download_slices(sst_plan* plan, int which, uint64_t first, uint64_t count, float* dst,
+                                       int dst_on_device, void* stream);
+
+/* ---- multi-slab driver in one process (SURVEY.md §8(b) sst_run_steps_multi) ----
+ * The global grid (desc->grid_dims, slowest..fastest) is cut along its slowest axis
+ * into nslabs slabs, slab i on device devs[i] (several slabs may share a device;
+ * neighbours on different GPUs must be peer-accessible, NVLink / NVSwitch). Every
+ * step is one launch per slab with the halo exchange fused into its epilogue (the
+ * sst_plan_set_peer stores) and stream flags between neighbours; the result equals
+ * the single-domain sweep bitwise. */
+typedef struct sst_multi sst_multi;
+SST_API sst_status sst_multi_create(const sst_plan_desc* desc, int nslabs, const int* devs, sst_multi** out);
+SST_API void sst_multi_destroy(sst_multi* m);
+/* dense global fp32 grid (host or device memory of the first slab's GPU) -> slabs */
+SST_API sst_status sst_multi_upload(sst_multi* m, const float* grid, int grid_on_device);
+/* enqueue `steps` time steps on the slabs' streams (asynchronous) */
+SST_API sst_status sst_multi_run(sst_multi* m, uint64_t steps);
+SST_API sst_status sst_multi_sync(sst_multi* m);
+/* slabs -> dense global grid (every owned slice, boundary ring included); synchronous */
+SST_API sst_status sst_multi_download(sst_multi* m, float* grid, int grid_on_device);
+/* slab i's plan, stream and owned global slices [owned[0], owned[1]) */
+SST_API sst_status sst_multi_slab(const sst_multi* m, int i, sst_plan** plan, void** stream, uint64_t owned[2]);
+/* One call: the stencil sweep of a host grid over ngpu slabs (direct_apply's
+ * contract, full-size output like sst_apply_host). */
+SST_API sst_status sst_run_steps_multi(const sst_plan_desc* desc, int ngpu, const int* devs, const float* h_in,
+                                       float* h_out, uint64_t steps);
 
 /* Profiling aid: when dev_buf (device memory, 4 x u64 per CTA) is non-NULL,
  * every following launch writes per CTA {smid, start ns, main-loop start ns,

@@ -107,6 +107,54 @@ Grid sparse_apply(const StencilSpec& spec, const Grid& grid, std::uint64_t steps
     return res;
 }
 
+// The same sweep slab-decomposed along the slowest axis over devices.size() slabs
+// (sst_run_steps_multi; several slabs may share a GPU, neighbours on different GPUs
+// must be peer-accessible): bitwise the single-domain result.
+template <class StencilSpec, class Grid>
+Grid sparse_apply_multi(const StencilSpec& spec, const Grid& grid, std::uint64_t steps,
+                        const std::vector<int>& devices, Precision precision = Precision::f16) {
+    if (steps == 0) throw std::invalid_argument("steps must be >= 1");
+    if (devices.empty()) throw std::invalid_argument("need at least one device");
+    if (grid.dims.size() != static_cast<std::size_t>(spec.dims))
+        throw std::invalid_argument("grid dimensionality does not match stencil");
+    const std::size_t k = static_cast<std::size_t>(spec.k), shrink = steps * (k - 1);
+    std::vector<std::uint64_t> dims(grid.dims.begin(), grid.dims.end());
+    std::size_t cells = 1;
+    for (auto d : dims) {
+        if (d < k + shrink - (k - 1)) throw std::invalid_argument("grid smaller than kernel");
+        cells *= static_cast<std::size_t>(d);
+    }
+    if (grid.values.size() != cells) throw std::invalid_argument("grid values do not match its dims");
+    const std::string doc = spec_document(spec);
+    sst_compiled* c = nullptr;
+    check(sst_compile(doc.c_str(), dims.data(), static_cast<int>(dims.size()), 16, 8, 1, &c));
+    std::unique_ptr<sst_compiled, void (*)(sst_compiled*)> cg(c, sst_compiled_destroy);
+    sst_plan_desc desc;
+    check(sst_compiled_plan_desc(c, &desc));
+    desc.precision = static_cast<int32_t>(precision);
+    std::vector<float> in(grid.values.begin(), grid.values.end()), out(cells);
+    check(sst_run_steps_multi(&desc, static_cast<int>(devices.size()), devices.data(), in.data(), out.data(),
+                              steps));
+    const std::size_t c0 = shrink / 2, nd = dims.size();
+    Grid res = grid;
+    res.dims.clear();
+    for (auto d : dims) res.dims.push_back(static_cast<std::size_t>(d) - shrink);
+    std::size_t n_out = 1;
+    for (auto d : res.dims) n_out *= d;
+    res.values.assign(n_out, 0.0);
+    std::vector<std::size_t> idx(nd, 0);
+    for (std::size_t flat = 0; flat < n_out; ++flat) {
+        std::size_t rem = flat, src = 0;
+        for (std::size_t a = nd; a-- > 0;) {
+            idx[a] = rem % res.dims[a];
+            rem /= res.dims[a];
+        }
+        for (std::size_t a = 0; a < nd; ++a) src = src * static_cast<std::size_t>(dims[a]) + idx[a] + c0;
+        res.values[flat] = static_cast<double>(out[src]);
+    }
+    return res;
+}
+
 }  // namespace sst
 
 #endif  // SPARSTENCIL_HPP_

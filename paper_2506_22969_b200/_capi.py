@@ -27,6 +27,8 @@ EXPORTED = [
     "sst_compile_result_summary", "sst_compile_result_report", "sst_compile_result_lut", "sst_explore",
     "sst_plan_set_peer", "sst_plan_buffers", "sst_device_alloc", "sst_device_free", "sst_ipc_handle",
     "sst_ipc_open", "sst_ipc_close", "sst_stream_write_u32", "sst_stream_wait_geq_u32",
+    "sst_run_steps_peer", "sst_download_slices", "sst_multi_create", "sst_multi_destroy", "sst_multi_upload",
+    "sst_multi_run", "sst_multi_sync", "sst_multi_download", "sst_multi_slab", "sst_run_steps_multi",
 ]
 
 
@@ -162,6 +164,16 @@ def lib() -> C.CDLL:
         "sst_ipc_close": (i32, [P]),
         "sst_stream_write_u32": (i32, [P, P, C.c_uint32]),
         "sst_stream_wait_geq_u32": (i32, [P, P, C.c_uint32]),
+        "sst_run_steps_peer": (i32, [P, i32, u64, P, P, P, P, C.c_uint32, C.POINTER(i32)]),
+        "sst_download_slices": (i32, [P, i32, u64, u64, P, i32, P]),
+        "sst_multi_create": (i32, [C.POINTER(PlanDesc), i32, C.POINTER(i32), C.POINTER(P)]),
+        "sst_multi_destroy": (None, [P]),
+        "sst_multi_upload": (i32, [P, P, i32]),
+        "sst_multi_run": (i32, [P, u64]),
+        "sst_multi_sync": (i32, [P]),
+        "sst_multi_download": (i32, [P, P, i32]),
+        "sst_multi_slab": (i32, [P, i32, C.POINTER(P), C.POINTER(P), C.POINTER(u64)]),
+        "sst_run_steps_multi": (i32, [C.POINTER(PlanDesc), i32, C.POINTER(i32), P, P, u64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -111,4 +111,9 @@ void launch_ring_to_half(const float* src, __half* d0, __half* d1, int gx, int g
                          long long rp, long long pp, int lp, long long rph, long long pph, int lph,
                          cudaStream_t st);
 
+// Stream-ordered flag write / wait >= (cuStreamWriteValue32 / cuStreamWaitValue32,
+// resolved at run time through the driver entry points; runtime.cu).
+void stream_write(cudaStream_t st, uint32_t* dev_addr, uint32_t value);
+void stream_wait_geq(cudaStream_t st, uint32_t* dev_addr, uint32_t value);
+
 }  // namespace sstl

@@ -1069,6 +1069,32 @@ sst_status sst_download(sst_plan* plan, int which, float* dst, int dst_on_device
     }
 }
 
+sst_status sst_download_slices(sst_plan* plan, int which, uint64_t first, uint64_t count, float* dst,
+                               int dst_on_device, void* stream) {
+    try {
+        if (!plan || !dst) throw std::invalid_argument("null argument");
+        if (which < 0 || which > 1) throw std::invalid_argument("buffer index must be 0 or 1");
+        if (!plan->buf[0]) throw std::invalid_argument("plan has no bound buffers");
+        if (plan->fold_n) throw std::invalid_argument("slices of a 1D fold");
+        const uint64_t slices = static_cast<uint64_t>(plan->dims == 3 ? plan->gz : plan->gy);
+        if (first + count > slices) throw std::out_of_range("slice range beyond the grid");
+        ck(cudaSetDevice(plan->device), "cudaSetDevice");
+        const auto st = static_cast<cudaStream_t>(stream);
+        const size_t w = static_cast<size_t>(plan->gx) * 4;
+        const size_t rows_per_slice = plan->dims == 3 ? static_cast<size_t>(plan->gy) : 1;
+        const size_t pitch = plan->storage.row_pitch * 4;
+        const float* base = plan->buf[which] + plan->storage.left_pad +
+                            static_cast<int64_t>(first) * static_cast<int64_t>(rows_per_slice) *
+                                static_cast<int64_t>(plan->storage.row_pitch);
+        ck(cudaMemcpy2DAsync(dst, w, base, pitch, w, static_cast<size_t>(count) * rows_per_slice,
+                             dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st),
+           "cudaMemcpy2DAsync(download slices)");
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
 sst_status sst_plan_set_trace(sst_plan* plan, void* dev_buf) {
     try {
         if (!plan) throw std::invalid_argument("null plan");
@@ -1177,12 +1203,25 @@ StreamValueFn stream_fn(const char* name) {
 }
 }  // namespace
 
+extern "C++" {
+void sstl::stream_write(cudaStream_t st, uint32_t* dev_addr, uint32_t value) {
+    static StreamValueFn fn = stream_fn("cuStreamWriteValue32");
+    const CUresult rc = fn(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(dev_addr), value,
+                           CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (rc != CUDA_SUCCESS) throw CudaError("cuStreamWriteValue32 failed (" + std::to_string(rc) + ")", false);
+}
+
+void sstl::stream_wait_geq(cudaStream_t st, uint32_t* dev_addr, uint32_t value) {
+    static StreamValueFn fn = stream_fn("cuStreamWaitValue32");
+    const CUresult rc = fn(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(dev_addr), value,
+                           CU_STREAM_WAIT_VALUE_GEQ);
+    if (rc != CUDA_SUCCESS) throw CudaError("cuStreamWaitValue32 failed (" + std::to_string(rc) + ")", false);
+}
+}  // extern "C++"
+
 sst_status sst_stream_write_u32(void* stream, uint32_t* dev_addr, uint32_t value) {
     try {
-        static StreamValueFn fn = stream_fn("cuStreamWriteValue32");
-        const CUresult rc = fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(dev_addr), value,
-                               CU_STREAM_WRITE_VALUE_DEFAULT);
-        if (rc != CUDA_SUCCESS) throw CudaError("cuStreamWriteValue32 failed (" + std::to_string(rc) + ")", false);
+        sstl::stream_write(static_cast<cudaStream_t>(stream), dev_addr, value);
         return SST_OK;
     } catch (...) {
         return sstc::from_current_exception();
@@ -1191,10 +1230,7 @@ sst_status sst_stream_write_u32(void* stream, uint32_t* dev_addr, uint32_t value
 
 sst_status sst_stream_wait_geq_u32(void* stream, uint32_t* dev_addr, uint32_t value) {
     try {
-        static StreamValueFn fn = stream_fn("cuStreamWaitValue32");
-        const CUresult rc = fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(dev_addr), value,
-                               CU_STREAM_WAIT_VALUE_GEQ);
-        if (rc != CUDA_SUCCESS) throw CudaError("cuStreamWaitValue32 failed (" + std::to_string(rc) + ")", false);
+        sstl::stream_wait_geq(static_cast<cudaStream_t>(stream), dev_addr, value);
         return SST_OK;
     } catch (...) {
         return sstc::from_current_exception();
@@ -1238,6 +1274,37 @@ sst_status sst_run_steps(sst_plan* plan, int src, uint64_t steps, void* stream, 
         if (steps % plan->fuse != 0)
             throw std::invalid_argument("steps must be a multiple of the fusion factor");
         const int cur = plan->launch(src, steps / plan->fuse, st);
+        if (dst_out) *dst_out = cur;
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_run_steps_peer(sst_plan* plan, int src, uint64_t steps, void* stream, uint32_t* my_flags,
+                              uint32_t* up_flag, uint32_t* down_flag, uint32_t launch0, int* dst_out) {
+    try {
+        if (!plan) throw std::invalid_argument("null plan");
+        if (src < 0 || src > 1) throw std::invalid_argument("buffer index must be 0 or 1");
+        if (!plan->tmap_ok) throw std::invalid_argument("plan has no bound buffers");
+        if (steps % plan->fuse != 0) throw std::invalid_argument("steps must be a multiple of the fusion factor");
+        const bool up = plan->peer_buf[0][0] != nullptr, down = plan->peer_buf[1][0] != nullptr;
+        if ((up && !up_flag) || (down && !down_flag) || ((up || down) && !my_flags))
+            throw std::invalid_argument("peer flags missing");
+        ck(cudaSetDevice(plan->device), "cudaSetDevice");
+        const auto st = static_cast<cudaStream_t>(stream);
+        int cur = src;
+        const uint64_t launches = steps / plan->fuse;
+        for (uint64_t i = 0; i < launches; ++i) {
+            const uint32_t u = launch0 + static_cast<uint32_t>(i);
+            // both neighbours finished launch u - 1: this launch's input halos are in
+            // place and they no longer read the buffers its halo stores go to
+            if (up) sstl::stream_wait_geq(st, my_flags + 0, u);
+            if (down) sstl::stream_wait_geq(st, my_flags + 1, u);
+            cur = plan->launch(cur, 1, st);
+            if (up) sstl::stream_write(st, up_flag, u + 1);
+            if (down) sstl::stream_write(st, down_flag, u + 1);
+        }
         if (dst_out) *dst_out = cur;
         return SST_OK;
     } catch (...) {

@@ -190,6 +190,91 @@ class SparseStencil:
             pass
 
 
+class MultiSlabStencil:
+    """A compiled stencil slab-decomposed over several slabs in one process
+    (sst_multi_*): slab i on device devices[i] (several may share a GPU), halos
+    fused into each slab's epilogue (P2P stores), neighbours ordered by stream flags."""
+
+    def __init__(self, stencil: str, grid_dims: Sequence[int], devices: Sequence[int], fuse: int = 1,
+                 precision: str = "f16"):
+        if precision not in PRECISIONS:
+            raise _capi.InvalidArgument(f"precision must be one of {sorted(PRECISIONS)}")
+        self.compiled = Compiled(stencil, grid_dims, 16, 8, fuse)
+        self.grid_dims = self.compiled.grid_dims
+        desc = self.compiled.plan_desc()
+        desc.precision = PRECISIONS[precision]
+        self.fuse = max(1, int(desc.fuse))
+        self.r = (int(self.compiled.info["k"]) - 1) // 2 // self.fuse
+        self.devices = [int(d) for d in devices]
+        devs = (C.c_int * len(self.devices))(*self.devices)
+        h = C.c_void_p()
+        check(lib().sst_multi_create(C.byref(desc), len(self.devices), devs, C.byref(h)))
+        self._h = h
+
+    def slab(self, i: int) -> dict:
+        plan, stream = C.c_void_p(), C.c_void_p()
+        owned = (C.c_uint64 * 2)()
+        check(lib().sst_multi_slab(self._h, int(i), C.byref(plan), C.byref(stream), owned))
+        s = _capi.PlanStats()
+        check(lib().sst_plan_stats_get(plan, C.byref(s)))
+        return {"owned": (owned[0], owned[1]), "stream": stream.value, "plan": plan.value,
+                "launches": int(s.launches)}
+
+    def upload(self, grid):
+        on_dev, ptr, keep = _pointer(grid)
+        check(lib().sst_multi_upload(self._h, C.c_void_p(ptr), int(on_dev)))
+        return keep
+
+    def run(self, steps: int):
+        check(lib().sst_multi_run(self._h, int(steps)))
+
+    def sync(self):
+        check(lib().sst_multi_sync(self._h))
+
+    def download(self, out=None):
+        if out is None:
+            out = np.empty(self.grid_dims, dtype=np.float32)
+        on_dev, ptr, _ = _pointer(out)
+        check(lib().sst_multi_download(self._h, C.c_void_p(ptr), int(on_dev)))
+        return out
+
+    def apply_host(self, grid: np.ndarray, steps: int) -> np.ndarray:
+        self.upload(np.ascontiguousarray(grid, dtype=np.float32))
+        self.run(steps)
+        return self.download()
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().sst_multi_destroy(self._h)
+            self._h = None
+        if getattr(self, "compiled", None) is not None:
+            self.compiled.close()
+            self.compiled = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_steps_multi(stencil: str, grid: np.ndarray, steps: int, devices: Sequence[int],
+                    precision: str = "f16") -> np.ndarray:
+    """sst_run_steps_multi: one call, full-size result (like SparseStencil.apply_host)."""
+    g = np.ascontiguousarray(grid, dtype=np.float32)
+    comp = Compiled(stencil, list(g.shape), 16, 8, 1)
+    try:
+        desc = comp.plan_desc()
+        desc.precision = PRECISIONS[precision]
+        devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+        out = np.empty_like(g)
+        check(lib().sst_run_steps_multi(C.byref(desc), len(devices), devs, g.ctypes.data_as(C.c_void_p),
+                                        out.ctypes.data_as(C.c_void_p), int(steps)))
+        return out
+    finally:
+        comp.close()
+
+
 def _pointer(arr):
     """(on_device, address, keepalive) for numpy arrays and torch tensors."""
     if isinstance(arr, np.ndarray):

@@ -254,20 +254,22 @@ class SlabStencil:
             torch.cuda.synchronize(torch.device("cuda", self.device))
             dist.barrier(group=self.group)
 
-    def _step_p2p(self, stream):
+    def _steps_p2p(self, steps, stream):
+        """The per-step schedule in C (sst_run_steps_peer): for each launch u, wait
+        until both neighbours finished launch u - 1 (flag words in this rank's memory),
+        launch, then write u + 1 into the neighbours' flag words."""
         import ctypes as C
 
         from ._capi import check, lib
 
-        L = lib()
-        u = self._launch
-        for which in self._peer_flag:  # both neighbours finished launch u - 1
-            check(L.sst_stream_wait_geq_u32(C.c_void_p(stream or None), C.c_void_p(self._flags + 4 * which),
-                                            u))
-        self.cur = self.eng.run(self.fuse, src=self.cur, stream=stream)
-        for which, addr in self._peer_flag.items():
-            check(L.sst_stream_write_u32(C.c_void_p(stream or None), C.c_void_p(addr), u + 1))
-        self._launch = u + 1
+        dst = C.c_int()
+        up = self._peer_flag.get(0)
+        down = self._peer_flag.get(1)
+        check(lib().sst_run_steps_peer(self.eng._h, self.cur, int(steps), C.c_void_p(stream or None),
+                                       C.c_void_p(self._flags), C.c_void_p(up), C.c_void_p(down),
+                                       self._launch, C.byref(dst)))
+        self.cur = dst.value
+        self._launch += steps // self.fuse
 
     # -- data --------------------------------------------------------------
     def make_local_input(self, seed: int = 1):
@@ -330,8 +332,7 @@ class SlabStencil:
             raise ValueError("steps must be a multiple of the fusion factor")
         if self.halo == "p2p":
             self.eng.set_row_window(0, 0)
-            for _ in range(steps // self.fuse):
-                self._step_p2p(stream)
+            self._steps_p2p(steps, stream)
             return
         for _ in range(steps // self.fuse):
             works = exchange_halos(self.layout, self.flat[self.cur], self.pitch, self.group)

@@ -383,6 +383,13 @@ static void perf_tests() {
     const auto t = explore_layouts_tcgen05(hw_preset("b200-sparse"), stencil_preset("Box-2D9P"),
                                            std::array<std::size_t, 2>{8192, 8192}, 128);
     CHECK(t.best.r1 * t.best.r2 == 128 && t.best.r1 == 16);
+    // tall-narrow grids: the model may rank (8, 16) first, but the choice is the
+    // layout sst_plan_create runs
+    for (const auto& g : {std::vector<std::size_t>{8000, 40}, std::vector<std::size_t>{8000, 40, 20}}) {
+        const auto s = stencil_preset(g.size() == 2 ? "Box-2D9P" : "Box-3D27P");
+        const auto e = explore_layouts_tcgen05(hw_preset("b200-sparse"), s, g, 128);
+        CHECK(e.best.r1 == 16 && e.best.r2 == 8 && device_runnable(e.best.r1, e.best.r2));
+    }
 }
 
 // Emulate the sm_100a kernel's data path on the CPU from the device image the
