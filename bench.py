@@ -15,8 +15,13 @@ Default --steps 1000 times the config's full 1000-step run.
   cpu_baseline  the reference's own direct_apply (oracle/_ref, built from the
              reference sources) on the host cores, bounded sample
 
-N > 1 (torchrun): weak scaling, each rank owns an 8192-row slab of a
-(8192*N) x 8192 global grid; halo rows are exchanged with NCCL every step.
+N > 1 (torchrun): the north-star scaling config by default — Box-3D27P 1024^3
+STRONG-scaled: rank i owns 1024/N planes (+ 1 halo plane per neighbour); each step
+is one launch per rank whose epilogue also stores the boundary planes straight into
+the neighbours' halo planes over NVLink (P2P, CUDA IPC), ranks ordered by stream
+flags by the C per-step schedule (sst_run_steps_peer). Rank 0 also times the same
+1024^3 grid alone on its GPU (`n1_same_grid`) so the line carries its own N = 1
+reference. `--config X --weak` keeps the old weak scaling (X per rank).
 
 --impl reference: the reference CPU implementation (oracle/_ref) on the host
 cores, same metric; each step is one time step over a bounded row band.
@@ -250,17 +255,33 @@ def run_engine(args, cfg, cfg_name):
 
     from paper_2506_22969_b200 import SparseStencil
 
-    stencil, dims, _ = cfg
+    stencil, global_dims, _ = cfg
     ws, rank, local = _dist_env()
+    if args.share_gpu:  # functional runs of the multi-rank path on a one-GPU host
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
-    # weak scaling: each rank owns a slab of `dims` rows (plus halo rows)
+        if args.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     from paper_2506_22969_b200.multigpu import SlabStencil
 
+    strong = ws > 1 and not args.weak
+    if strong:  # rank-owned slab of the global grid (slowest axis split N ways)
+        if global_dims[0] % ws:
+            raise SystemExit(f"{global_dims[0]} slices do not split over {ws} ranks")
+        dims = (global_dims[0] // ws, *global_dims[1:])
+    else:
+        dims = global_dims
+    n1 = None
+    if strong and rank == 0:  # the same global grid on this GPU alone (N = 1 reference)
+        n1 = _n1_same_grid(stencil, global_dims, local, args)
+    if ws > 1:
+        dist.barrier()
     eng = SlabStencil(stencil, dims, rank=rank, world=ws, device=local, fuse=args.fuse,
                       precision=args.precision, halo=args.halo)
     grid = eng.make_local_input(seed=1)  # dense fp32 torch tensor on the device
@@ -338,7 +359,7 @@ def run_engine(args, cfg, cfg_name):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    cells_global = int(np.prod(dims)) * ws
+    cells_global = int(np.prod(dims)) * ws  # (strong: = the global grid)
     value = args.steps * cells_global / (ms / 1e3) / 1e9
 
     # roofline of the dominant kernel: one launch reads the grid and writes the
@@ -400,13 +421,18 @@ def run_engine(args, cfg, cfg_name):
             dist.destroy_process_group()
         return
     cpu = None if (ws > 1 or args.no_cpu) else cpu_baseline(stencil, dims)
+    workload = (f"{stencil} {'x'.join(map(str, global_dims))} strong-scaled over {ws} GPUs "
+                f"({dims[0]} planes each + halos), {args.steps} time steps (one bench step = one time step)"
+                if strong else
+                f"{stencil} {'x'.join(map(str, dims))} per GPU, {args.steps} time steps "
+                f"(one bench step = one time step)")
     line = {
         "metric": METRIC, "value": value, "unit": "GStencil/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+        "dtype": "f16",
         "data": "synthetic (random_grid seed 1: dyadic values in [0,1))",
-        "config": {"workload": f"{stencil} {'x'.join(map(str, dims))} per GPU, "
-                               f"{args.steps} time steps (one bench step = one time step)",
+        "config": {"workload": workload, "global_grid": list(global_dims) if strong else None,
                    "stencil": stencil, "grid_per_gpu": list(dims), "time_steps": args.steps,
                    "temporal_fusion": args.fuse,
                    "storage": ("fp32 input / output, binary16 between steps (bitwise the fp32-storage result: "
@@ -441,9 +467,37 @@ def run_engine(args, cfg, cfg_name):
         "gpu_launches": int(launches),
         "clocks": clk,
     }
+    if n1 is not None:
+        line["n1_same_grid"] = n1
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
+
+
+def _n1_same_grid(stencil, global_dims, device, args):
+    """The strong-scaled global grid on one GPU (rank 0's), same steps: the N = 1
+    point of the scaling curve, measured in the same run."""
+    import torch
+
+    from paper_2506_22969_b200.multigpu import SlabStencil
+
+    eng = SlabStencil(stencil, global_dims, device=device, fuse=args.fuse, precision=args.precision)
+    eng.load(eng.make_local_input(seed=1))
+    eng.step(args.warmup * args.fuse)
+    stream = torch.cuda.current_stream(torch.device("cuda", device))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(device)
+    a.record(stream)
+    eng.step(args.steps)
+    b.record(stream)
+    torch.cuda.synchronize(device)
+    ms = a.elapsed_time(b)
+    eng.close()
+    del eng
+    torch.cuda.empty_cache()
+    return {"value": args.steps * int(np.prod(global_dims)) / (ms / 1e3) / 1e9, "unit": "GStencil/s",
+            "ms_per_step": ms / args.steps, "n_gpus": 1,
+            "note": "the same global grid and steps on rank 0's GPU alone (the N = 1 point of this strong scaling)"}
 
 
 def main():
@@ -452,11 +506,16 @@ def main():
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
-    ap.add_argument("--config", default="box2d", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="default: box2d (BASELINE configs[1]) on one GPU, box3d1024 strong-scaled for N > 1")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--halo", default="nccl", choices=["nccl", "p2p"],
+    ap.add_argument("--weak", action="store_true",
+                    help="N > 1: weak scaling (the config's grid per rank) instead of strong scaling")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="N > 1 on a one-GPU host: every rank on device 0, gloo control plane (functional)")
+    ap.add_argument("--halo", default="p2p", choices=["nccl", "p2p"],
                     help="multi-GPU halo exchange: NCCL p2p overlapped with the interior window, or fused "
                          "into the kernel (boundary slices stored into the neighbours' buffers over NVLink)")
     ap.add_argument("--precision", default="f16", choices=["f16", "f16x2"],
@@ -464,6 +523,8 @@ def main():
     ap.add_argument("--fuse", type=int, default=1,
                     help="temporal fusion factor (reference fuse_time_steps); steps count original time steps")
     args = ap.parse_args()
+    if args.config is None:
+        args.config = "box3d1024" if int(os.environ.get("WORLD_SIZE", "1")) > 1 and not args.weak else "box2d"
     cfg = CONFIGS[args.config]
     if args.steps is None:
         args.steps = cfg[2]

@@ -51,3 +51,33 @@ def test_small_grid_line(gpu):
     assert roof["bound"] == "hbm" and 0.2 < roof["frac"] < 1.3
     assert roof["l2_flushed_single_launch"]["ms_per_launch"] > 0
     assert "sm_mhz" in line["clocks"]
+
+
+def test_default_config_per_world_size():
+    """N = 1 runs BASELINE configs[1] (Box-2D9P 8192^2); N > 1 the north-star scaling
+    config (Box-3D27P 1024^3 strong-scaled, P2P halos) unless --weak."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    assert b.CONFIGS["box2d"][:2] == ("Box-2D9P", (8192, 8192))
+    assert b.CONFIGS["box3d1024"][:2] == ("Box-3D27P", (1024, 1024, 1024))
+    for n in (2, 4, 8):  # strong scaling: whole planes per rank, >= 2 halo widths each
+        assert 1024 % n == 0 and 1024 // n >= 2
+
+
+@pytest.mark.gpu
+def test_two_rank_strong_scaling_line_shared_gpu():
+    """torchrun, 2 ranks sharing the one GPU (gloo control plane, IPC P2P halos):
+    the strong-scaling line with its own N = 1 reference (functional, not a timing)."""
+    res = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py", "--gpus", "2",
+                          "--share-gpu", "--config", "box3d", "--steps", "4", "--warmup", "3"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-3000:]
+    line = json.loads([x for x in res.stdout.strip().splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["config"]["global_grid"] == [512, 512, 512] and line["config"]["grid_per_gpu"] == [256, 512, 512]
+    assert line["n1_same_grid"]["value"] > 0 and line["gpu_launches"] == 4
+    assert "p2p" in line["config"]["parallelism"]
