@@ -589,7 +589,9 @@ struct sst_plan {
             p.sched = dyn ? d_sched : nullptr;
             p.sched_base = sched_base;
             h16.launch(dyn, hi, ho, grid, hi ? smem_h : smem_f32_h, st, m, p);
-            if (dyn) sched_base += static_cast<uint32_t>(p.nbatch + grid * (sst::kDrawAhead - 1));
+            if (dyn)
+                sched_base += static_cast<uint32_t>((p.nbatch + sst::kDrawGroup - 1) / sst::kDrawGroup +
+                                                    grid * (sst::kDrawAhead - 1));
             ck(cudaGetLastError(), "kernel launch");
             ++launches;
             ++h16_launches;
@@ -692,7 +694,9 @@ struct sst_plan {
             variant->launch(grid, smem, st, maps, p, multi && !mdyn);
             // (items - grid draws, plus one final draw per CTA)
             if (dyn)
-                sched_base += static_cast<uint32_t>(p.nbatch * (mdyn ? chunk : 1) + grid * (sst::kDrawAhead - 1));
+                sched_base += static_cast<uint32_t>(
+                    (p.nbatch * (mdyn ? chunk : 1) + sst::kDrawGroup - 1) / sst::kDrawGroup +
+                    grid * (sst::kDrawAhead - 1));
             ck(cudaGetLastError(), "kernel launch");
             ++launches;
             if (mdyn) {  // per-batch step counters

@@ -224,6 +224,20 @@ __device__ __forceinline__ void tmem_ld_32x32b_x8(uint32_t taddr, uint32_t (&r)[
         : "r"(taddr));
 }
 
+// warp-collective .16x256b shape (layout pinned by tools/probes/probe_tmem_shapes.cu):
+// 16 lanes from taddr's lane; thread t of the warp receives, per 8-column block b,
+// {(lane t/4, col 8b + 2(t%4)), (t/4, 8b + 2(t%4) + 1), (t/4 + 8, 8b + 2(t%4)),
+//  (t/4 + 8, 8b + 2(t%4) + 1)} in r[4b .. 4b + 3].
+__device__ __forceinline__ void tmem_ld_16x256b_x4(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.16x256b.x4.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+
 // ------------------------------------------------------- UMMA descriptors
 // SM100 shared-memory matrix descriptor, SWIZZLE_NONE (interleaved core
 // matrices of 8 rows x 16 bytes). lbo/sbo in bytes.

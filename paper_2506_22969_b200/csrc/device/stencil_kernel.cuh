@@ -77,6 +77,7 @@ __host__ __device__ inline SmemLayout smem_layout_generic(int nks, int k_pad, in
 // rings, 3 + 2 + 2 deep).
 constexpr int kBidSlots = 16;
 constexpr int kDrawAhead = 2;  // dynamic scheduling: counter draws in flight per CTA
+constexpr int kDrawGroup = 2;  // consecutive batches (items) per counter draw
 // dynamic multi-step mode: items committed but not yet published (publication every
 // kPubEvery items, lagging kPubLag store groups)
 constexpr int kPubEvery = 8, kPubLag = 2, kPubRing = 16;
@@ -288,14 +289,23 @@ __global__ void __launch_bounds__(kThreads, CPS)
             // patches: loads-only ablation 3.3 TB/s). Consuming slots in draw order
             // keeps the counter exact: each consumed batch triggers one draw, so a
             // launch advances it by nitems + G * (kDrawAhead - 1), and the first
-            // invalid slot a CTA meets is followed only by invalid ones.
+            // invalid slot a CTA meets is followed only by invalid ones. With groups of
+            // kDrawGroup batches per draw the count is in groups: ceil(nitems / kDrawGroup).
             uint32_t q0 = blockIdx.x, q1 = 0;
             if (lane == 0) q1 = static_cast<uint32_t>(G) + atomicAdd(p.sched, 1u) - p.sched_base;
+            // one draw covers kDrawGroup consecutive batches (fewer same-address atomics)
             auto item = [&](uint32_t& slot) -> bool {
+                uint32_t grp = 0;
+                if (lane == 0) {
+                    grp = slot;
+                    if (grp * static_cast<uint32_t>(kDrawGroup) < static_cast<uint32_t>(nitems))
+                        slot = static_cast<uint32_t>(G) + atomicAdd(p.sched, 1u) - p.sched_base;
+                }
+                for (int e = 0; e < kDrawGroup; ++e) {
                 int g = -1;
                 if (lane == 0) {
-                    g = slot < static_cast<uint32_t>(nitems) ? static_cast<int>(slot) : -1;
-                    if (g >= 0) slot = static_cast<uint32_t>(G) + atomicAdd(p.sched, 1u) - p.sched_base;
+                    const uint32_t gi = grp * static_cast<uint32_t>(kDrawGroup) + static_cast<uint32_t>(e);
+                    g = gi < static_cast<uint32_t>(nitems) ? static_cast<int>(gi) : -1;
                     sBid[r % kBidSlots] = g;
                     mbar_arrive(&bid_full[r % kBidSlots]);
                 }
@@ -333,6 +343,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
                 }
                 __syncwarp();
                 ++r;
+                }
                 return true;
             };
             while (item(q0) && item(q1)) {
