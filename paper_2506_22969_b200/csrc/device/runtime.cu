@@ -127,6 +127,7 @@ Variant make_stream_variant() {
         raise_smem_attr(sst::stencil3d_stream_kernel<TYB, NP, KZ, NB, NACC, NS, AT, true>, smem);
     };
     v.multistep = false;
+    v.h16c = sstl::typed_fns_3d(TYB, NP, KZ, AT, NB, NACC, NS);
     v.launch = [](int grid, int smem, cudaStream_t st, const sst::MapSet& maps, const sst::StepParams& p,
                   bool coop) {
         if (p.peer_mask)
@@ -282,6 +283,7 @@ struct sst_plan {
     int load_x0_h = 0;
     __half* hbuf[2] = {nullptr, nullptr};
     CUtensorMap hin[2]{}, hout[2]{};  // f16 patch loads / interior stores
+    CUtensorMap hring[2]{};           // 3D: the f16 buffers' right-edge ring chunks (kEdgeRing)
     bool hmaps_ok = false;
     uint64_t h16_launches = 0;        // launches that read or wrote binary16 storage
 
@@ -525,6 +527,8 @@ struct sst_plan {
         }
         const cuuint64_t gstride[2] = {storage_h.row_pitch * 2, storage_h.plane_pitch * 2};
         const int ox = gx - 2 * r, ox8 = ox & ~7;
+        // the 3D stream kernel stores the whole last 16-byte chunk (kEdgeRing)
+        const int oxs = (variant->kz > 0 && (ox & 7)) ? ox8 + 8 : ox8;
         for (int i = 0; i < 2; ++i) {
             const cuuint64_t gdim[3] = {storage_h.row_pitch, static_cast<cuuint64_t>(gy), static_cast<cuuint64_t>(gz)};
             const cuuint32_t box[3] = {static_cast<cuuint32_t>(img_h.geo.patch_w),
@@ -535,11 +539,16 @@ struct sst_plan {
             __half* base = hbuf[i] + (dims == 3 ? r * static_cast<int64_t>(storage_h.plane_pitch) : 0) +
                            static_cast<int64_t>(r) * static_cast<int64_t>(storage_h.row_pitch) +
                            static_cast<int64_t>(storage_h.left_pad) + r;
-            const cuuint64_t odim[3] = {static_cast<cuuint64_t>(std::max(ox8, 8)),
+            const cuuint64_t odim[3] = {static_cast<cuuint64_t>(std::max(oxs, 8)),
                                         static_cast<cuuint64_t>(gy - 2 * r), static_cast<cuuint64_t>(gz - 2 * r)};
             const cuuint32_t obox[3] = {64u, static_cast<cuuint32_t>(tiles_y * sst::kTileH), 1u};
             encode(&hout[i], dims, base, odim, gstride, obox, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+            if (dims == 3) {
+                const cuuint32_t rbox[3] = {8u, static_cast<cuuint32_t>(tiles_y * sst::kTileH), 1u};
+                encode(&hring[i], 3, hbuf[i], gdim, gstride, rbox, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+            }
         }
         hmaps_ok = true;
     }
@@ -563,6 +572,9 @@ struct sst_plan {
             sst::MapSet m{};
             m.in[0] = m.in[1] = hi ? hin[(t - 1) & 1] : maps.in[src];
             m.out[0] = m.out[1] = ho ? hout[t & 1] : maps.out[fin];
+            // 3D: the output storage's ring chunks (binary16: the output buffer's own,
+            // converted from buf[src]; fp32: the input buffer's, never rewritten)
+            m.ring[0] = m.ring[1] = ho ? hring[t & 1] : maps.ring[src];
             float* outp = ho ? reinterpret_cast<float*>(hbuf[t & 1]) : buf[fin];
             p.src = 0;
             p.buf[0] = p.buf[1] = outp;
@@ -580,7 +592,9 @@ struct sst_plan {
             }
             const char* dyn_e = std::getenv("SST_DYN");
             // (the store-only ablation, debug bit 32, has no producer to draw batches)
-            const bool dyn = !(debug_mode & 32) && (dyn_e ? std::atoi(dyn_e) != 0 : p.nbatch >= 8 * grid);
+            // (the 3D stream kernel splits its work statically)
+            const bool dyn = variant->kz == 0 && !(debug_mode & 32) &&
+                             (dyn_e ? std::atoi(dyn_e) != 0 : p.nbatch >= 8 * grid);
             if (dyn && !d_sched) {
                 ck(cudaMalloc(&d_sched, 4), "cudaMalloc(sched)");
                 ck(cudaMemsetAsync(d_sched, 0, 4, st), "cudaMemsetAsync(sched)");
@@ -878,11 +892,19 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
             P->storage.bytes = (cells + 3) / 4 * 4 * 4;
         }
 
-        // binary16 inter-step storage: f16 operands only, 2D full-grid runs (see launch)
+        // binary16 inter-step storage: f16 operands only, full-grid runs (see launch)
         if (terms == 1 && !P->fold_n && !P->variant->h16c.empty()) {
-            const uint64_t lph = (8 - static_cast<uint64_t>(P->r) % 8) % 8;  // interior starts 16-byte aligned
+            // the interior starts 16-byte aligned (2D) / 128-byte aligned (3D: whole-sector
+            // TMA stores, as for the fp32 storage)
+            const uint64_t alh = d->dims == 3 ? 64 : 8;  // elements
+            const uint64_t lph = (alh - static_cast<uint64_t>(P->r) % alh) % alh;
             P->storage_h.left_pad = lph;
-            P->storage_h.row_pitch = (lph + static_cast<uint64_t>(P->gx) + 7) / 8 * 8;
+            P->storage_h.row_pitch = (lph + static_cast<uint64_t>(P->gx) + alh - 1) / alh * alh;
+            {  // room for the 3D stream kernel's full last 16-byte store chunk
+                const uint64_t ox = static_cast<uint64_t>(P->gx - 2 * P->r);
+                const uint64_t need = lph + static_cast<uint64_t>(P->r) + (ox + 7) / 8 * 8;
+                if (P->storage_h.row_pitch < need) P->storage_h.row_pitch = (need + alh - 1) / alh * alh;
+            }
             P->storage_h.plane_pitch = P->storage_h.row_pitch * static_cast<uint64_t>(P->gy);
             P->storage_h.bytes = P->storage_h.plane_pitch * static_cast<uint64_t>(P->gz) * 2;
             P->load_x0_h = static_cast<int>(lph & ~uint64_t{7});

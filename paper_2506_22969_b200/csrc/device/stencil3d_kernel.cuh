@@ -35,12 +35,15 @@ __host__ __device__ constexpr int ring_slots() {
     return NP + NB + NACC + 1 <= 16 ? 16 : 32;
 }
 
+// elem: patch element bytes (4 fp32 storage, 2 binary16 inter-step storage). A ring
+// slot is 16 bytes per output row in both cases (4 fp32 or 8 binary16 cells).
 template <int TYB, int NP, int KZ, int NB, int NACC, int NS, bool AT>
-__host__ __device__ inline SmemLayout smem_layout_stream(int nks, int k_pad, int patch_w, int patch_h) {
+__host__ __device__ inline SmemLayout smem_layout_stream(int nks, int k_pad, int patch_w, int patch_h,
+                                                         int elem = 4) {
     constexpr int kRingSlots = ring_slots<NP, NB, NACC>();
     static_assert(kRingSlots > NP + NB + NACC, "ring cache slots vs pipeline depth");
     SmemLayout L = smem_layout_generic<TYB>(nks, k_pad, patch_w, patch_h, 1, NP, NB,
-                                            2 * NP + 2 * NB + 2 * NACC + kRingSlots, NS, AT);
+                                            2 * NP + 2 * NB + 2 * NACC + kRingSlots, NS, AT, elem);
     L.ring = align_up(L.total, 16);
     L.total = align_up(L.ring + static_cast<uint32_t>(kRingSlots * TYB * kTileH * 4 * 4), 128);
     return L;
@@ -72,7 +75,14 @@ __device__ __forceinline__ void for_each_run(int u0, int u1, int ozw, int nby, i
 // AT: compressed A'' in TMEM instead of smem (frees smem and its bandwidth: with
 // N = 32 the per-MMA A reads were the largest smem stream of the 3D kernel).
 // PEER: the slab P2P halo stores are compiled in (launched only when p.peer_mask != 0)
-template <int TYB, int NP, int KZ, int NB, int NACC, int NS, bool AT, bool PEER = false>
+// HIN / HOUT: the input / output grid is binary16 storage (SST_PREC_F16 runs keep steps
+// 1 .. T-1 in binary16, see typed2d.cuh): binary16 patches are gathered by copying the
+// bits, binary16 outputs are rounded RNE in the epilogue. The right-edge ring cache
+// always holds the OUTPUT storage's ring chunk (maps.ring[p.src] then maps the output
+// buffer: its ring cells are constant and equal to the input's): 4 fp32 or 8 binary16
+// cells per row, 16 bytes either way.
+template <int TYB, int NP, int KZ, int NB, int NACC, int NS, bool AT, bool PEER = false, bool HIN = false,
+          bool HOUT = false>
 __global__ void __launch_bounds__(kThreads, 1)
     stencil3d_stream_kernel(const __grid_constant__ MapSet maps, const StepParams p) {
     constexpr int N = kTXB * TYB;
@@ -85,10 +95,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     static_assert(NACC > KZ, "one accumulator beyond the KZ open ones");
     static_assert(N % 16 == 0 && N <= 128, "UMMA N for M=128");
     static_assert(NACC * N <= 320, "accumulator ring must leave TMEM room for metadata / A''");
+    static_assert(!(PEER && (HIN || HOUT)), "slab peers use fp32 storage");
+    constexpr int ELEM = HIN ? 2 : 4;   // patch element bytes
+    constexpr int RW = HOUT ? 8 : 4;    // cells per 16-byte output chunk (ring cache row)
     using namespace ptx;
 
     extern __shared__ __align__(1024) uint8_t smem[];
-    const SmemLayout L = smem_layout_stream<TYB, NP, KZ, NB, NACC, NS, AT>(p.nks, p.k_pad, p.patch_w, p.patch_h);
+    const SmemLayout L =
+        smem_layout_stream<TYB, NP, KZ, NB, NACC, NS, AT>(p.nks, p.k_pad, p.patch_w, p.patch_h, ELEM);
     uint8_t* sA = smem + L.a;
     uint8_t* sB = smem + L.b;
     uint8_t* sS = smem + L.s;
@@ -103,7 +117,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* d_full = b_full + 2 * NB;
     uint64_t* d_empty = d_full + NACC;
     uint64_t* ring_full = d_empty + NACC;  // [kRingSlots]
-    float* sRing = reinterpret_cast<float*>(smem + L.ring);
+    uint8_t* sRing = smem + L.ring;  // [kRingSlots][TYB*8 rows][16 bytes]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.tmem_slot);
 
     const int warp = threadIdx.x / 32;
@@ -177,9 +191,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 && !(p.debug_mode & 32)) {
         // ------------------------------------------------------ TMA producer
         if (elect_one()) {
-            const uint32_t pbytes = static_cast<uint32_t>(p.patch_w * p.patch_h) * 4u;
-            const int ox = p.gx - 2 * p.r, ox4 = ox & ~3;
-            const bool edge = ox4 != ox && bx * (kTXB * kTileW) + kTXB * kTileW > ox && !(p.debug_mode & 24);
+            const uint32_t pbytes = static_cast<uint32_t>(p.patch_w * p.patch_h * ELEM);
+            const int ox = p.gx - 2 * p.r, oxc = ox & ~(RW - 1);
+            const bool edge = oxc != ox && bx * (kTXB * kTileW) + kTXB * kTileW > ox && !(p.debug_mode & 24);
             int it = 0;
             for_each_run(u0, u1, ozw, p.nby, p.zchunk, [&](int col, int zo_a, int zo_b) {
                 int X0, Y0;
@@ -194,11 +208,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     mbar_arrive_expect_tx(&patch_full[s], pbytes);
                     tma_load_3d(sP + s * L.p_stride, tmap_in, &patch_full[s], X0 + p.load_x0, Y0, z);
-                    if (edge) {  // right-edge chunk [ox4, ox4 + 4) of the TYB*8 output rows
+                    if (edge) {  // right-edge chunk [oxc, oxc + RW) of the TYB*8 output rows
                         const int rs = it % kRingSlots;
-                        mbar_arrive_expect_tx(&ring_full[rs], static_cast<uint32_t>(TYB * kTileH * 4 * 4));
-                        tma_load_3d(sRing + rs * (TYB * kTileH * 4), &maps.ring[p.src], &ring_full[rs],
-                                    static_cast<int>(p.left_pad) + p.r + ox4, Y0 + p.r, z);
+                        mbar_arrive_expect_tx(&ring_full[rs], static_cast<uint32_t>(TYB * kTileH * 16));
+                        tma_load_3d(sRing + rs * (TYB * kTileH * 16), &maps.ring[p.src], &ring_full[rs],
+                                    static_cast<int>(p.left_pad) + p.r + oxc, Y0 + p.r, z);
                     }
                 }
             });
@@ -266,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int gw = warp - kGatherWarp0;
         const bool active = gw < NGROUP;
         int32_t toff[GPW][8];
-        tile_offsets<TYB, GPW>(gw, p.patch_w, toff);
+        tile_offsets<TYB, GPW, ELEM>(gw, p.patch_w, toff);
         const uint32_t gstride = static_cast<uint32_t>(p.k_pad) * 16u;
         const int nsweeps = (active && !(p.debug_mode & 2)) ? ksz : 0;
         int it = 0;
@@ -276,8 +290,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int ps = it % NP, s = it % NB;
                 mbar_wait(&patch_full[ps], (it / NP) & 1);
                 mbar_wait(&b_empty[s], ((it / NB) & 1) ^ 1);
-                gather_batch<GPW>(smem_u32(sP + ps * L.p_stride), smem_u32(sB + s * L.b_stride),
-                                  sGsrc, sGdst, nsweeps, gw, gstride, lane, toff, p.lo_sweep0);
+                gather_batch<GPW, HIN>(smem_u32(sP + ps * L.p_stride), smem_u32(sB + s * L.b_stride),
+                                       sGsrc, sGdst, nsweeps, gw, gstride, lane, toff, p.lo_sweep0);
 
                 fence_proxy_async_smem();
                 __syncwarp();
@@ -291,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int etid = threadIdx.x - kEpiWarp0 * 32;
         int o = 0, it_base = 0;  // it_base: gather iteration of the run's first input plane
         const int ox = p.gx - 2 * p.r;
-        const bool edge = (ox & 3) != 0 && bx * (kTXB * kTileW) + kTXB * kTileW > ox && !(p.debug_mode & 24);
+        const bool edge = (ox & (RW - 1)) != 0 && bx * (kTXB * kTileW) + kTXB * kTileW > ox && !(p.debug_mode & 24);
         for_each_run(u0, u1, ozw, p.nby, p.zchunk, [&](int col, int zo_a, int zo_b) {
             int X0, Y0;
             col_xy(col, X0, Y0);
@@ -311,16 +325,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&d_empty[slot]);
                 }
-                const float* ring = nullptr;
+                const uint8_t* ring = nullptr;
                 if (edge && !(p.debug_mode & 32)) {  // center input plane of output zo
                     const int ci = it_base + (zo - zo_a) + R;
                     mbar_wait(&ring_full[ci % kRingSlots], (ci / kRingSlots) & 1);
-                    ring = sRing + (ci % kRingSlots) * (TYB * kTileH * 4);
+                    ring = sRing + (ci % kRingSlots) * (TYB * kTileH * 16);
                 }
-                if (!(p.debug_mode & 1))
+                if constexpr (HOUT) {
+                    if (!(p.debug_mode & 1))
+                        store_batch_h<3, TYB, NS, kEdgeRing>(p, tmap_out,
+                                                             reinterpret_cast<__half*>(buf_of(p, p.src ^ 1)), v, sS,
+                                                             L.s_stride, o, X0, Y0, p.slow_lo + zo, q, lane, etid,
+                                                             reinterpret_cast<const __half*>(ring));
+                } else if (!(p.debug_mode & 1))
                     store_batch<3, TYB, NS, kEdgeRing, PEER>(
                         p, tmap_out, buf_of(p, p.src ^ 1), v, sS, L.s_stride, o, X0, Y0, p.slow_lo + zo, q, lane,
-                        etid, ring, (p.peer_mask & 1) ? &p.peer_maps->up[p.src ^ 1] : nullptr,
+                        etid, reinterpret_cast<const float*>(ring), (p.peer_mask & 1) ? &p.peer_maps->up[p.src ^ 1] : nullptr,
                         (p.peer_mask & 2) ? &p.peer_maps->down[p.src ^ 1] : nullptr);
             }
             it_base += zo_b - zo_a + 1 + 2 * R;

@@ -543,18 +543,39 @@ __device__ __forceinline__ void store_right_edge_h(const StepParams& p, __half* 
         }
 }
 
-template <int DIMS, int TYB, int NS>
+// EDGE = kEdgeRing (3D stream kernel): as in store_batch, no plain stores; the store
+// map runs to ox8 + 8 and the cells [ox, ox8 + 8) of that last 16-byte chunk are
+// staged with the output storage's own (constant) binary16 values from `ring`
+// (TYB*8 rows x 8 halves).
+template <int DIMS, int TYB, int NS, int EDGE = kEdgePlain>
 __device__ __forceinline__ void store_batch_h(const StepParams& p, const CUtensorMap* tmap_out, __half* dst,
-                                              const uint32_t (&v)[kTXB / 2][2 * TYB], uint8_t* sS,
+                                              uint32_t (&v)[kTXB / 2][2 * TYB], uint8_t* sS,
                                               uint32_t s_stride, int nb, int X0, int Y0, int Z0, uint32_t q,
-                                              uint32_t lane, int etid) {
+                                              uint32_t lane, int etid, const __half* ring = nullptr) {
     using namespace ptx;
     constexpr int CW = 2 * TYB, NBOX = kTXB / 2;
     constexpr int HBOX = 64;  // halves per 128-byte box row
     const uint32_t dy = lane % 8;
     const uint32_t inchunk = ((q & 1u) * 4u + lane / 8u) * 2u;  // byte of dx % 8 inside its 16 B chunk
     const int ox = p.gx - 2 * p.r, ox8 = ox & ~7;
-    store_right_edge_h<DIMS, TYB>(p, dst, v, X0, Y0, Z0, q, lane);
+    const int oxs = (EDGE == kEdgeRing && ox8 != ox) ? ox8 + 8 : ox8;  // store map end (exclusive)
+    if constexpr (EDGE == kEdgePlain) {
+        store_right_edge_h<DIMS, TYB>(p, dst, v, X0, Y0, Z0, q, lane);
+    } else if (ring != nullptr && X0 + kTXB * kTileW > ox) {
+        const int dxl = static_cast<int>(q) * 4 + static_cast<int>(lane / 8);
+#pragma unroll
+        for (int c = 0; c < NBOX; ++c)
+#pragma unroll
+            for (int par = 0; par < 2; ++par) {
+                const int xr = X0 + c * kBoxW + par * kTileW + dxl;
+                if (xr >= ox && xr < oxs) {
+#pragma unroll
+                    for (int ty = 0; ty < TYB; ++ty)  // exact: binary16 -> f32 -> binary16
+                        v[c][2 * ty + par] =
+                            __float_as_uint(__half2float(ring[(ty * kTileH + static_cast<int>(dy)) * 8 + (xr - ox8)]));
+                }
+            }
+    }
     // a binary16 batch fills half an fp32 staging slot: 2 NS buffers, so the TMA
     // stores of batch n read one while batch n + 1 stages into the next
     constexpr int NSH = 2 * NS;
@@ -582,7 +603,7 @@ __device__ __forceinline__ void store_batch_h(const StepParams& p, const CUtenso
 #pragma unroll
         for (int cb = 0; cb < NBOX / 2; ++cb) {
             const int bx0 = X0 + cb * HBOX;
-            if (bx0 >= ox8) break;  // fully clipped
+            if (bx0 >= oxs) break;  // fully clipped
             if (DIMS == 2)
                 tma_store_2d(tmap_out, sS + buf + cb * s_stride, bx0, Y0 - p.slow_lo);
             else

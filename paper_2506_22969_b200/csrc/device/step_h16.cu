@@ -25,6 +25,4 @@ std::vector<TypedFns> typed_fns_2d(int tyb, int np, bool a_tmem, int ns, int cps
     return v;
 }
 
-std::vector<TypedFns> typed_fns_3d(int, int, int, bool, int, int, int) { return {}; }
-
 }  // namespace sstl

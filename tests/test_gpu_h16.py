@@ -108,3 +108,62 @@ def test_h16_run_steps_device_buffers(gpu):
         finally:
             os.environ.pop("SST_H16", None)
             eng.close()
+
+
+# ---------------------------------------------------------------- 3D z-streaming kernel
+@pytest.mark.parametrize("name", ["Heat-3D", "Box-3D27P"])
+@pytest.mark.parametrize("dims", [(20, 24, 40), (9, 9, 9), (13, 70, 131), (34, 33, 262), (11, 40, 517)])
+@pytest.mark.parametrize("steps", [2, 5])
+def test_h16_3d_bitwise_equals_f32_storage(gpu, name, dims, steps):
+    """Ragged right edges of every residue mod 8 (the binary16 store map's last
+    16-byte chunk carries ring / pad cells staged from the ring cache)."""
+    g = oracle.random_grid(dims, seed=21).astype(np.float32)
+    ref, got, _ = run_both(name, g, steps)
+    assert np.array_equal(ref.view(np.uint32), got.view(np.uint32))
+
+
+@pytest.mark.parametrize("gx", [37, 38, 39, 40, 41, 42, 43, 44])
+def test_h16_3d_every_edge_residue(gpu, gx):
+    g = oracle.random_grid((12, 19, gx), seed=gx).astype(np.float32)
+    ref, got, _ = run_both("Box-3D27P", g, 3)
+    assert np.array_equal(ref.view(np.uint32), got.view(np.uint32))
+
+
+def test_h16_3d_matches_round16_oracle(gpu):
+    g = oracle.random_grid((40, 48, 70), seed=4)
+    ref, got, eng = run_both("Box-3D27P", g.astype(np.float32), 6)
+    core = valid_core(got, 6, eng.r).astype(np.float64)
+    assert np.array_equal(core, oracle.direct_apply_mt("Box-3D27P", g, 6, round16=True))
+
+
+def test_h16_3d_full_size_box3d(gpu):
+    """BASELINE configs[3] grid: Box-3D27P 512^3, 6 steps, whole grid bitwise."""
+    g = oracle.random_grid((512, 512, 512), seed=1).astype(np.float32)
+    ref, got, _ = run_both("Box-3D27P", g, 6)
+    assert np.array_equal(ref.view(np.uint32), got.view(np.uint32))
+
+
+def test_h16_3d_run_steps_device_buffers(gpu):
+    import torch
+
+    g = oracle.random_grid((18, 30, 77), seed=17).astype(np.float32)
+    want = {}
+    for h16 in ("0", "1"):
+        os.environ["SST_H16"] = h16
+        eng = SparseStencil("Heat-3D", [18, 30, 77])
+        try:
+            eng.bind()
+            for src in (0, 1):
+                for steps in (2, 3):
+                    eng.upload(torch.from_numpy(g).cuda(), src)
+                    torch.cuda.synchronize()
+                    dst = eng.run(steps, src)
+                    assert dst == (src + steps) & 1
+                    out = eng.download(dst)
+                    if h16 == "0":
+                        want[(src, steps)] = out
+                    else:
+                        assert np.array_equal(out.view(np.uint32), want[(src, steps)].view(np.uint32))
+        finally:
+            os.environ.pop("SST_H16", None)
+            eng.close()
