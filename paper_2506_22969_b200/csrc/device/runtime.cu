@@ -286,6 +286,13 @@ struct sst_plan {
     CUtensorMap hring[2]{};           // 3D: the f16 buffers' right-edge ring chunks (kEdgeRing)
     bool hmaps_ok = false;
     uint64_t h16_launches = 0;        // launches that read or wrote binary16 storage
+    int variant_index = -1;
+    // 3D: binary16 runs go through a companion plan over the SAME fp32 buffers built
+    // for the variant that is fastest with binary16 storage (TYB = 8: N = 64 MMAs,
+    // half the MMA issues per output; Box-3D27P 512^3 146 vs 180 us per step), while
+    // this plan keeps the variant that is fastest for fp32 single steps (TYB = 4:
+    // 194 vs 224 us), which the slab / peer paths use
+    std::unique_ptr<sst_plan> typed;
 
     ~sst_plan() {
         cudaSetDevice(device);
@@ -648,8 +655,15 @@ struct sst_plan {
         const bool multi = ms_env && variant->multistep && full && nsteps > 1 && !fold_n && !peer_buf[0][0] &&
                            !peer_buf[1][0];
         const bool mdyn = multi && ms_dyn;
-        if (h16_ok && h16_enabled() && !multi && full && nsteps > 1 && !peer_buf[0][0] && !peer_buf[1][0])
-            return launch_h16(src, nsteps, st);
+        if ((typed ? typed->h16_ok : h16_ok) && h16_enabled() && !multi && full && nsteps > 1 && !peer_buf[0][0] &&
+            !peer_buf[1][0]) {
+            if (!typed) return launch_h16(src, nsteps, st);
+            const uint64_t l0 = typed->launches, h0 = typed->h16_launches;
+            const int fin = typed->launch_h16(src, nsteps, st);
+            launches += typed->launches - l0;
+            h16_launches += typed->h16_launches - h0;
+            return fin;
+        }
         const int grid = grid_size(p, multi && !mdyn);
         if (multi && flags_n < p.nbatch) {
             cudaFree(d_flags);
@@ -734,10 +748,9 @@ int sst_device_count(void) {
     return n;
 }
 
-sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
-    try {
-        if (!d || !out) throw std::invalid_argument("null argument");
-        *out = nullptr;
+namespace {
+// forced_variant >= 0: only that variant (else SST_VARIANT or the preference order)
+std::unique_ptr<sst_plan> create_plan(const sst_plan_desc* d, int device, int forced_variant) {
         if (d->precision != SST_PREC_F16 && d->precision != SST_PREC_F16X2)
             throw std::invalid_argument("unsupported precision");
         const int terms = d->precision == SST_PREC_F16X2 ? 2 : 1;
@@ -821,7 +834,7 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
         int nvar = 0;
         const Variant* vars = variants(nvar);
         const char* force = std::getenv("SST_VARIANT");
-        const int forced = force ? std::atoi(force) : -1;
+        const int forced = forced_variant >= 0 ? forced_variant : force ? std::atoi(force) : -1;
         const char* asm_env = std::getenv("SST_A_SMEM");
         const bool no_a_tmem = asm_env && std::atoi(asm_env) != 0;
         for (int i = 0; i < nvar && !P->variant; ++i) {
@@ -844,6 +857,7 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
             if (v.ctas_per_sm > 1 && tneed > 512u / static_cast<uint32_t>(v.ctas_per_sm)) continue;
             if (sst::prologue_scratch_bytes(nks, v.a_tmem) > L.gsrc - L.b) continue;
             P->variant = &v;
+            P->variant_index = i;
             P->smem = need;
             P->tmem_cols = tneed <= 32 ? 32 : tneed <= 64 ? 64 : tneed <= 128 ? 128 : tneed <= 256 ? 256 : 512;
             geo.tiles_y = v.tyb;
@@ -961,6 +975,34 @@ sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
         ck(cudaMemcpy(P->d_gdst, P->img.gather_dst.data(), P->img.gather_dst.size() * 4,
                       cudaMemcpyHostToDevice),
            "cudaMemcpy");
+        return P;
+}
+
+// 3D z-streaming variants in preference order for binary16 runs (see sst_plan::typed)
+constexpr int kTyped3D[] = {12, 10};
+}  // namespace
+
+sst_status sst_plan_create(const sst_plan_desc* d, int device, sst_plan** out) {
+    try {
+        if (!d || !out) throw std::invalid_argument("null argument");
+        *out = nullptr;
+        auto P = create_plan(d, device, -1);
+        const char* sub_e = std::getenv("SST_H16_SUBPLAN");
+        if (P->dims == 3 && P->variant->kz > 0 && !P->fold_n && !std::getenv("SST_VARIANT") &&
+            !(sub_e && std::atoi(sub_e) == 0) && d->precision == SST_PREC_F16) {
+            for (const int vi : kTyped3D) {
+                if (vi == P->variant_index) break;  // the plan's own variant is the typed choice
+                std::unique_ptr<sst_plan> T;
+                try {
+                    T = create_plan(d, device, vi);
+                } catch (const std::invalid_argument&) {
+                    continue;  // does not fit this stencil
+                }
+                if (!T->h16_ok || T->variant->kz != P->variant->kz) continue;
+                P->typed = std::move(T);
+                break;
+            }
+        }
         *out = P.release();
         return SST_OK;
     } catch (...) {
@@ -1000,8 +1042,9 @@ sst_status sst_plan_stats_get(const sst_plan* plan, sst_plan_stats* s) {
         s->ctas = plan->grid_size(p);
         s->launches = plan->launches;
         s->h16_launches = plan->h16_launches;
-        s->h16_capable = plan->h16_ok ? 1 : 0;
-        s->h16_patch_stages = plan->h16_ok ? plan->h16.np_h16 * 100 + plan->h16.nbb * 10 + plan->h16.nacc : 0;
+        const sst_plan* hp = plan->typed ? plan->typed.get() : plan;  // the plan binary16 runs use
+        s->h16_capable = hp->h16_ok ? 1 : 0;
+        s->h16_patch_stages = hp->h16_ok ? hp->h16.np_h16 * 100 + hp->h16.nbb * 10 + hp->h16.nacc : 0;
         return SST_OK;
     } catch (...) {
         return sstc::from_current_exception();
@@ -1039,7 +1082,14 @@ sst_status sst_plan_bind(sst_plan* plan, void* b0, void* b1) {
         ck(cudaMemset(plan->buf[1], 0, plan->storage.bytes), "cudaMemset");
         plan->make_tmaps();
         // binary16 storage pair up front (not inside the first timed run)
-        if (plan->h16_ok) plan->ensure_h16();
+        if (plan->typed) {  // the companion plan works on the same fp32 buffers
+            plan->typed->buf[0] = plan->buf[0];
+            plan->typed->buf[1] = plan->buf[1];
+            plan->typed->make_tmaps();
+            plan->typed->ensure_h16();
+        } else if (plan->h16_ok) {
+            plan->ensure_h16();
+        }
         return SST_OK;
     } catch (...) {
         return sstc::from_current_exception();
@@ -1125,6 +1175,7 @@ sst_status sst_plan_set_trace(sst_plan* plan, void* dev_buf) {
     try {
         if (!plan) throw std::invalid_argument("null plan");
         plan->trace = static_cast<unsigned long long*>(dev_buf);
+        if (plan->typed) plan->typed->trace = plan->trace;
         return SST_OK;
     } catch (...) {
         return sstc::from_current_exception();
