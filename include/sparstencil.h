@@ -299,6 +299,16 @@ SST_API sst_status sst_compile_result_lut(const sst_compile_result* r, uint8_t* 
 SST_API sst_status sst_explore(const char* stencil, const uint64_t* grid_dims, int ndims, const char* hw,
                                uint64_t fuse, int r_max, double* buf, size_t cap, size_t* len);
 
+/* Engine execution model (stensor::estimate_device, hwmodel.hpp; an extension of
+ * the reference's perf model): predicted time of ONE launch of the sm_100a kernels
+ * applying `stencil` (fused `fuse` times) on the device layout (16, 8) to a grid.
+ * storage: 2 = binary16 between steps (a run of >= 2 steps), 4 = fp32. tyb: tiles
+ * per batch along y, 0 = what the runtime picks (2D: 4; 3D: 8 binary16 / 4 fp32).
+ * out[12] = {updates, batches, hbm_bytes, smem_wavefronts, mma_issues, t_hbm, t_smem,
+ * t_mma, t_total (s), GStencil/s, bound (0 hbm, 1 smem, 2 tensor), k_pad}. */
+SST_API sst_status sst_estimate_device(const char* stencil, const uint64_t* grid_dims, int ndims, uint64_t fuse,
+                                       int storage, int tyb, double out[12]);
+
 /* ----------------------------------------------------------------- misc */
 /* Synthetic input: stensor::random_grid (stencil.hpp:84-85; mt19937_64(seed),
  * (x & 0xff) / 256, dyadic and exact in fp32), written as fp32. */

@@ -77,6 +77,7 @@ def ref() -> C.CDLL:
         L.ref_hier_match.argtypes = [u64, u64, i32, P, sz, C.POINTER(sz), C.POINTER(u64),
                                      C.POINTER(C.c_int)]
         L.ref_estimate.argtypes = [C.c_char_p, i32, P, i32, i32, i32, P, C.POINTER(u64)]
+        L.ref_estimate_hw_text.argtypes = [C.c_char_p, i32, P, i32, i32, i32, P, C.POINTER(u64)]
         _ref = L
     return _ref
 

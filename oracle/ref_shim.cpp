@@ -205,4 +205,23 @@ int ref_estimate(const char* hw, int dims, const uint64_t* grid, int k, int r1, 
     }
 }
 
+// the reference's own .hw parser (perf.cpp:93-134) on a descriptor text, then its
+// estimate (perf.cpp:39-70): pins presets/b200-sparse.hw against the reference model
+int ref_estimate_hw_text(const char* hw_text, int dims, const uint64_t* grid, int k, int r1, int r2,
+                         double* out4, uint64_t* n_mma_out) {
+    try {
+        std::vector<std::size_t> d(grid, grid + dims);
+        const auto e = estimate(parse_hw_descriptor(hw_text), dims, d, k, r1, r2);
+        out4[0] = e.t_compute;
+        out4[1] = e.t_memory;
+        out4[2] = e.t_total;
+        out4[3] = static_cast<double>(e.n_prime);
+        *n_mma_out = e.n_mma;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
 }  // extern "C"

@@ -11,6 +11,9 @@
 //   sstensor presets
 //   sstensor run     --stencil S --grid G --steps T [--fuse F] [--seed N] [--device D]
 //                    (engine extension: the B200 time loop, GStencil/s)
+//   sstensor model   --stencil S --grid G [--fuse T] [--storage f16|f32] [--tyb N]
+//                    (engine extension: the B200 execution model of one launch,
+//                    hwmodel.hpp estimate_device; no device needed)
 //
 // compile / verify run the desk-scale verification on the GPU (the reference
 // emulates it on the CPU); --no-verify skips it.
@@ -56,10 +59,11 @@ Args parse(int argc, char** argv) {
         {"verify", {"hw", "precision", "seed", "device"}},
         {"presets", {}},
         {"run", {"stencil", "grid", "steps", "fuse", "seed", "device"}},
+        {"model", {"stencil", "grid", "fuse", "storage", "tyb"}},
     };
     static const std::map<std::string, std::set<std::string>> kFlags = {
         {"compile", {"corrupt-permutation", "no-verify"}}, {"verify", {"no-verify"}}};
-    if (argc < 2) throw UsageError("a subcommand is required: compile | explore | verify | presets | run");
+    if (argc < 2) throw UsageError("a subcommand is required: compile | explore | verify | presets | run | model");
     Args a;
     a.cmd = argv[1];
     if (!kOpts.count(a.cmd)) throw UsageError("unknown subcommand: " + a.cmd);
@@ -186,6 +190,26 @@ int cmd_run(const Args& a) {
     return 0;
 }
 
+int cmd_model(const Args& a) {
+    if (!a.has("stencil") || !a.has("grid")) throw UsageError("model needs --stencil --grid");
+    const auto dims = parse_grid(a.get("grid"));
+    const std::string st = a.get("stencil");
+    const std::string text = stensor::is_preset(st) ? st : slurp(st);
+    const std::string storage = a.get("storage", "f16");
+    if (storage != "f16" && storage != "f32") throw UsageError("--storage must be f16 or f32");
+    std::vector<uint64_t> d(dims.begin(), dims.end());
+    double o[12];
+    ck(sst_estimate_device(text.c_str(), d.data(), static_cast<int>(d.size()), std::stoull(a.get("fuse", "1")),
+                           storage == "f16" ? 2 : 4, std::stoi(a.get("tyb", "0")), o));
+    static const char* kBound[] = {"hbm", "smem", "tensor"};
+    std::printf("updates %.0f  batches %.0f  k_pad %.0f\n", o[0], o[1], o[11]);
+    std::printf("hbm %.1f MB -> %.2f us | smem %.0f wavefronts -> %.2f us | tensor %.0f issues -> %.2f us\n",
+                o[2] / 1e6, o[5] * 1e6, o[3], o[6] * 1e6, o[4], o[7] * 1e6);
+    std::printf("predicted %.2f us per launch, %.1f GStencil/s, bound: %s\n", o[8] * 1e6, o[9],
+                kBound[static_cast<int>(o[10])]);
+    return 0;
+}
+
 int run(const Args& a) {
     if (a.cmd == "presets") {
         for (const auto& n : stensor::preset_names()) {
@@ -197,6 +221,7 @@ int run(const Args& a) {
         return 0;
     }
     if (a.cmd == "run") return cmd_run(a);
+    if (a.cmd == "model") return cmd_model(a);
     const auto hw = load_hw(a.get("hw", "a100-sparse"));
     const auto prec = parse_precision(a.get("precision", "exact64"));
     const std::uint64_t seed = std::stoull(a.get("seed", "1"));

@@ -1,6 +1,7 @@
 // C ABI, compile tier: host-only entry points (no GPU needed). The compile
 // order mirrors the reference pipeline (proj/core/src/pipeline.cpp:56-78, 112):
 // fuse -> choose (r1, r2) -> flatten -> crush -> convert_layout -> compress_24.
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -358,6 +359,32 @@ sst_status sst_explore(const char* stencil, const uint64_t* grid_dims, int ndims
                              double(e.m_prime), double(e.k_prime), double(e.n_prime)})
                 v.push_back(x);
         return copy_out(v, buf, cap, len);
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_estimate_device(const char* stencil, const uint64_t* grid_dims, int ndims, uint64_t fuse,
+                               int storage, int tyb, double out[12]) {
+    try {
+        if (!out) throw std::invalid_argument("null argument");
+        if (storage != 2 && storage != 4) throw std::invalid_argument("storage must be 2 (binary16) or 4 (fp32)");
+        sst_compiled* c = nullptr;
+        sst_status st = sst_compile(stencil, grid_dims, ndims, 16, 8, fuse, &c);
+        if (st != SST_OK) return st;
+        std::unique_ptr<sst_compiled, void (*)(sst_compiled*)> hold(c, sst_compiled_destroy);
+        const auto& L = c->cv.converted;
+        const int dims = L.dims;  // 1D grids are folded into a 2D view by sst_compile
+        const int kz = dims == 3 && L.z_factor > 1 && L.a.cols % L.z_factor == 0 ? static_cast<int>(L.z_factor) : 1;
+        const int t = tyb > 0 ? tyb : (dims == 3 && storage == 2 ? 8 : 4);
+        const auto e = stensor::estimate_device(stensor::DeviceModel{}, dims, c->dims, c->spec.k, L.r1, L.r2,
+                                                L.a.cols, kz, t, storage, storage, static_cast<int>(c->fuse));
+        const double v[12] = {e.updates, e.batches, e.hbm_bytes, e.smem_wavefronts, e.mma_issues, e.t_hbm, e.t_smem,
+                              e.t_mma, e.t_total, e.gstencil,
+                              std::string(e.bound) == "hbm" ? 0.0 : std::string(e.bound) == "smem" ? 1.0 : 2.0,
+                              std::ceil(static_cast<double>(L.a.cols) / kz / 32.0) * 32.0};
+        std::memcpy(out, v, sizeof v);
+        return SST_OK;
     } catch (...) {
         return sstc::from_current_exception();
     }

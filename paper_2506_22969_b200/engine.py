@@ -374,3 +374,19 @@ def explore(stencil: str, grid_dims: Sequence[int], hw: str = "a100-sparse", fus
     rows = buf.reshape(-1, 9)
     return [{k: (int(v) if k in ("r1", "r2", "n_mma", "m_prime", "k_prime", "n_prime") else float(v))
              for k, v in zip(keys, r)} for r in rows]
+
+
+def estimate_device(stencil: str, grid_dims: Sequence[int], fuse: int = 1, storage: int = 2,
+                    tyb: int = 0) -> dict:
+    """The engine's execution model of one launch (stensor::estimate_device,
+    hwmodel.hpp): HBM, shared-memory pipe and tensor-pipe times on B200, the binding
+    one, and the predicted GStencil/s. storage: 2 binary16 between steps, 4 fp32."""
+    L = lib()
+    dims = (C.c_uint64 * len(grid_dims))(*[int(d) for d in grid_dims])
+    out = (C.c_double * 12)()
+    check(L.sst_estimate_device(stencil.encode(), dims, len(grid_dims), int(fuse), int(storage), int(tyb), out))
+    keys = ["updates", "batches", "hbm_bytes", "smem_wavefronts", "mma_issues", "t_hbm", "t_smem", "t_mma",
+            "t_total", "gstencil", "bound", "k_pad"]
+    d = dict(zip(keys, list(out)))
+    d["bound"] = ("hbm", "smem", "tensor")[int(d["bound"])]
+    return d

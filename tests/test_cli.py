@@ -81,3 +81,11 @@ def test_run_time_loop(gpu, stencil, grid):
     r = sst("run", "--stencil", stencil, "--grid", grid, "--steps", "50")
     assert r.returncode == 0, r.stderr
     assert "GStencil/s" in r.stdout and "launches" in r.stdout
+
+
+def test_model_subcommand():
+    r = sst("model", "--stencil", "Box-2D9P", "--grid", "8192x8192", "--storage", "f32")
+    assert r.returncode == 0, r.stderr
+    assert "bound: hbm" in r.stdout and "predicted" in r.stdout
+    r = sst("model", "--stencil", "Box-2D9P", "--grid", "8192x8192", "--storage", "f64")
+    assert r.returncode == 2
