@@ -469,9 +469,84 @@ def run_engine(args, cfg, cfg_name):
     }
     if n1 is not None:
         line["n1_same_grid"] = n1
+    # the engine's execution model of the dominant launch (hwmodel.hpp estimate_device):
+    # which on-chip resource binds when the HBM fraction is below 1
+    try:
+        from paper_2506_22969_b200 import estimate_device
+
+        m = estimate_device(stencil, dims, fuse=args.fuse, storage=2 if h16_launches else 4)
+        line["roofline"]["model"] = {"predicted_ms_per_launch": m["t_total"] * 1e3, "bound": m["bound"],
+                                     "t_hbm_ms": m["t_hbm"] * 1e3, "t_smem_ms": m["t_smem"] * 1e3,
+                                     "t_tensor_ms": m["t_mma"] * 1e3}
+    except Exception:
+        pass
+    if ws == 1 and not args.no_sweep and args.fuse == 1 and args.precision == "f16":
+        line["other_configs"] = _sweep_configs(args, cfg_name, local)
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
+
+
+def _sweep_configs(args, skip, device, budget_steps=60):
+    """Every other BASELINE config on this GPU in the same run (device-resident GStencil/s
+    at the config's operator, same timing rules as the headline: CUDA events on the
+    launch stream, grids whose ping-pong pair fits in L2 stepped round-robin over
+    independent copies). Steps per config: min(config T, budget_steps), one run of
+    binary16 inter-step storage for the large grids, as the headline."""
+    import torch
+
+    from paper_2506_22969_b200 import estimate_device
+    from paper_2506_22969_b200.multigpu import SlabStencil
+
+    out = {}
+    stream = torch.cuda.current_stream(torch.device("cuda", device))
+    peak, _ = _peaks()
+    for name, (stencil, dims, T) in CONFIGS.items():
+        if name == skip:
+            continue
+        steps = min(T, budget_steps)
+        pair = 2 * int(np.prod(dims)) * 4
+        small = pair <= 192 << 20
+        nrep = (-(-(400 << 20) // pair) + 1) if small else 1
+        engines = []
+        try:
+            for _ in range(nrep):
+                e = SlabStencil(stencil, dims, device=device)
+                e.load(e.make_local_input(seed=1))
+                engines.append(e)
+            engines[0].step(3)
+            for e in engines:
+                e.step(1)
+            torch.cuda.synchronize(device)
+            h0 = sum(int(e.eng.stats()["h16_launches"]) for e in engines)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            if small:
+                for i in range(steps):
+                    engines[i % nrep].step(1)
+            else:
+                engines[0].step(steps)
+            b.record(stream)
+            torch.cuda.synchronize(device)
+            ms = a.elapsed_time(b)
+            h16 = sum(int(e.eng.stats()["h16_launches"]) for e in engines) - h0
+            interior = engines[0].interior_cells()
+            alg = interior * (4.0 * steps + 4.0) if h16 else 8.0 * interior * steps
+            model = estimate_device(stencil, dims, storage=2 if h16 else 4)
+            out[name] = {"stencil": stencil, "grid": list(dims), "steps": steps, "config_T": T,
+                         "value": steps * int(np.prod(dims)) / (ms / 1e3) / 1e9, "unit": "GStencil/s",
+                         "ms_per_step": ms / steps, "storage": "binary16 between steps" if h16 else "fp32",
+                         "l2": f"{nrep} copies round-robin" if small else "grid pair > L2",
+                         "hbm_frac": alg / (ms / 1e3) / 1e9 / peak,
+                         "model": {"predicted_ms_per_step": model["t_total"] * 1e3, "bound": model["bound"]}}
+        except Exception as exc:  # a config that cannot run here must not sink the headline line
+            out[name] = {"error": str(exc)[:200]}
+        finally:
+            for e in engines:
+                e.close()
+            del engines
+            torch.cuda.empty_cache()
+    return out
 
 
 def _n1_same_grid(stencil, global_dims, device, args):
@@ -511,6 +586,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true",
+                    help="skip timing the other BASELINE configs (other_configs) after the headline")
     ap.add_argument("--weak", action="store_true",
                     help="N > 1: weak scaling (the config's grid per rank) instead of strong scaling")
     ap.add_argument("--share-gpu", action="store_true",

@@ -42,7 +42,7 @@ def test_steps_must_be_a_multiple_of_fuse():
 def test_small_grid_line(gpu):
     """Heat-2D 4096^2 (ping-pong pair < L2): timed over round-robin copies, the flushed
     single launch reported beside it, one launch per step, roofline and clocks present."""
-    res = _bench("--config", "heat2d", "--steps", "20", "--warmup", "3", "--no-cpu", "--no-e2e")
+    res = _bench("--config", "heat2d", "--steps", "20", "--warmup", "3", "--no-cpu", "--no-e2e", "--no-sweep")
     assert res.returncode == 0, res.stderr[-2000:]
     line = json.loads(res.stdout.strip().splitlines()[-1])
     assert line["gpu_launches"] == 20
@@ -81,3 +81,19 @@ def test_two_rank_strong_scaling_line_shared_gpu():
     assert line["config"]["global_grid"] == [512, 512, 512] and line["config"]["grid_per_gpu"] == [256, 512, 512]
     assert line["n1_same_grid"]["value"] > 0 and line["gpu_launches"] == 4
     assert "p2p" in line["config"]["parallelism"]
+
+
+@pytest.mark.gpu
+def test_default_line_times_every_other_config(gpu):
+    """The default line also times the other BASELINE configs (other_configs), each with
+    the engine model's prediction beside it."""
+    res = _bench("--steps", "6", "--warmup", "3", "--no-cpu", "--no-e2e", timeout=900)
+    assert res.returncode == 0, res.stderr[-2000:]
+    line = json.loads(res.stdout.strip().splitlines()[-1])
+    oc = line["other_configs"]
+    assert sorted(oc) == ["box3d", "box3d1024", "heat2d", "heat3d", "star2d"]
+    for name, v in oc.items():
+        assert "error" not in v, (name, v)
+        assert v["value"] > 0 and 0.05 < v["hbm_frac"] < 1.3
+        assert v["model"]["predicted_ms_per_step"] > 0
+    assert line["roofline"]["model"]["bound"] in ("hbm", "smem", "tensor")
