@@ -176,9 +176,30 @@ def cpu_baseline(stencil, dims, budget_s=12.0):
             break
     dt = time.perf_counter() - t0
     cells = n * int(np.prod(band))
-    return {"value": cells / dt / 1e9, "unit": "GStencil/s", "cores": threads, "kind": kind,
-            "sample": f"{n} x one time step of {stencil} on a {'x'.join(map(str, band))} band "
-                      f"of the {'x'.join(map(str, dims))} grid ({dt:.1f} s)"}
+    out = {"value": cells / dt / 1e9, "unit": "GStencil/s", "cores": threads, "kind": kind,
+           "sample": f"{n} x one time step of {stencil} on a {'x'.join(map(str, band))} band "
+                     f"of the {'x'.join(map(str, dims))} grid ({dt:.1f} s)"}
+    # BASELINE.md's plan beside it: the single-threaded reference on ONE pinned core over
+    # the FULL grid, one time step (grids up to 8192^2: a few seconds)
+    if kind == "reference" and int(np.prod(dims)) <= (1 << 26) + (1 << 20):
+        try:
+            full = oracle.random_grid(dims, seed=1)
+            aff = os.sched_getaffinity(0)
+            os.sched_setaffinity(0, {min(aff)})
+            try:
+                t0 = time.perf_counter()
+                oracle.ref_direct_apply_slabs(stencil, full, 1)
+                d1 = time.perf_counter() - t0
+            finally:
+                os.sched_setaffinity(0, aff)
+            out["single_core_full_grid"] = {
+                "value": int(np.prod(dims)) / d1 / 1e9, "unit": "GStencil/s", "cores": 1,
+                "sample": f"one time step of {stencil} over the whole {'x'.join(map(str, dims))} grid "
+                          f"({d1:.1f} s), the reference's direct_apply pinned to one core"}
+            del full
+        except Exception as exc:  # noqa: BLE001  (the headline must not depend on it)
+            out["single_core_full_grid"] = {"error": str(exc)[:200]}
+    return out
 
 
 def parity_check(stencil, host_in, host_out, steps, r, precision):
