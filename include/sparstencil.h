@@ -213,6 +213,15 @@ SST_API sst_status sst_ipc_close(void* dev_ptr);
 SST_API sst_status sst_stream_write_u32(void* stream, uint32_t* dev_addr, uint32_t value);
 SST_API sst_status sst_stream_wait_geq_u32(void* stream, uint32_t* dev_addr, uint32_t value);
 
+/* Several independent grids (one plan each, same device and fusion factor) stepped
+ * together: `steps` time steps of every plan, the launches interleaved step by step
+ * (step t of plans 0 .. n-1, then step t + 1). Per plan the result equals its own
+ * sst_run_steps; binary16 inter-step storage is used when every plan's run
+ * qualifies (full window, no peers, f16, >= 2 operator steps), else fp32 single
+ * steps. An ensemble of grids that each fit in L2 runs at the HBM-resident rate
+ * (bench.py's small-grid timing). dst_out[i]: buffer holding plan i's result. */
+SST_API sst_status sst_run_steps_batch(sst_plan* const* plans, int n, const int* src, uint64_t steps, void* stream,
+                                       int* dst_out);
 /* The per-step P2P schedule of one slab in C (what a rank of a multi-process run
  * calls instead of looping over sst_stream_wait_geq_u32 / sst_run_steps /
  * sst_stream_write_u32 itself): for launch u = launch0, launch0 + 1, ... wait until

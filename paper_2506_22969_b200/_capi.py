@@ -29,7 +29,7 @@ EXPORTED = [
     "sst_ipc_open", "sst_ipc_close", "sst_stream_write_u32", "sst_stream_wait_geq_u32",
     "sst_run_steps_peer", "sst_download_slices", "sst_multi_create", "sst_multi_destroy", "sst_multi_upload",
     "sst_multi_run", "sst_multi_sync", "sst_multi_download", "sst_multi_slab", "sst_run_steps_multi",
-    "sst_estimate_device",
+    "sst_estimate_device", "sst_run_steps_batch",
 ]
 
 
@@ -157,6 +157,7 @@ def lib() -> C.CDLL:
         "sst_compile_result_lut": (i32, [P, P, sz, C.POINTER(sz)]),
         "sst_explore": (i32, [C.c_char_p, C.POINTER(u64), i32, C.c_char_p, u64, i32, P, sz, C.POINTER(sz)]),
         "sst_estimate_device": (i32, [C.c_char_p, C.POINTER(u64), i32, u64, i32, i32, P]),
+        "sst_run_steps_batch": (i32, [C.POINTER(P), i32, C.POINTER(i32), u64, P, C.POINTER(i32)]),
         "sst_plan_set_peer": (i32, [P, i32, P, P, u64]),
         "sst_plan_buffers": (i32, [P, C.POINTER(P), C.POINTER(P)]),
         "sst_device_alloc": (i32, [i32, sz, C.POINTER(P)]),

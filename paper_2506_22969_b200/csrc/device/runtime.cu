@@ -575,7 +575,9 @@ struct sst_plan {
     // A run of nsteps >= 2 with binary16 inter-step storage: f32 buf[src] -> hbuf[0]
     // -> hbuf[1] -> ... -> f32 buf[(src + nsteps) & 1] (the index plain ping-pong
     // would end on; when that is buf[src] itself, step 1 read it long before).
-    int launch_h16(int src, uint64_t nsteps, cudaStream_t st) {
+    // h16_begin converts the ring; h16_step(t) issues launch t of the run (the batch
+    // driver, sst_run_steps_batch, interleaves the launches of several plans).
+    void h16_begin(int src, cudaStream_t st) {
         ensure_h16();
         sstl::launch_ring_to_half(buf[src], hbuf[0], hbuf[1], gx, gy, gz, r,
                                   static_cast<long long>(storage.row_pitch), static_cast<long long>(storage.plane_pitch),
@@ -583,53 +585,73 @@ struct sst_plan {
                                   static_cast<long long>(storage_h.plane_pitch), static_cast<int>(storage_h.left_pad),
                                   st);
         ck(cudaGetLastError(), "ring_to_half launch");
+    }
+
+    void h16_step(int src, uint64_t t, uint64_t nsteps, cudaStream_t st) {
         const int fin = static_cast<int>((static_cast<uint64_t>(src) + nsteps) & 1);
-        for (uint64_t t = 0; t < nsteps; ++t) {
-            const bool hi = t > 0, ho = t + 1 < nsteps;
-            sst::StepParams p = step_params(src);
-            const int grid = grid_size(p);
-            sst::MapSet m{};
-            m.in[0] = m.in[1] = hi ? hin[(t - 1) & 1] : maps.in[src];
-            m.out[0] = m.out[1] = ho ? hout[t & 1] : maps.out[fin];
-            // 3D: the output storage's ring chunks (binary16: the output buffer's own,
-            // converted from buf[src]; fp32: the input buffer's, never rewritten)
-            m.ring[0] = m.ring[1] = ho ? hring[t & 1] : maps.ring[src];
-            float* outp = ho ? reinterpret_cast<float*>(hbuf[t & 1]) : buf[fin];
-            p.src = 0;
-            p.buf[0] = p.buf[1] = outp;
-            p.tmem_cols = tmem_cols_h;
-            if (ho) {
-                p.row_pitch = static_cast<int64_t>(storage_h.row_pitch);
-                p.plane_pitch = static_cast<int64_t>(storage_h.plane_pitch);
-                p.left_pad = static_cast<int32_t>(storage_h.left_pad);
-            }
-            if (hi) {
-                p.load_x0 = load_x0_h;
-                p.patch_w = img_h.geo.patch_w;
-                p.gsrc = d_gsrc_h;
-                p.gdst = d_gdst_h;
-            }
-            const char* dyn_e = std::getenv("SST_DYN");
-            // (the store-only ablation, debug bit 32, has no producer to draw batches)
-            // (the 3D stream kernel splits its work statically)
-            const bool dyn = variant->kz == 0 && !(debug_mode & 32) &&
-                             (dyn_e ? std::atoi(dyn_e) != 0 : p.nbatch >= 8 * grid);
-            if (dyn && !d_sched) {
-                ck(cudaMalloc(&d_sched, 4), "cudaMalloc(sched)");
-                ck(cudaMemsetAsync(d_sched, 0, 4, st), "cudaMemsetAsync(sched)");
-                sched_base = 0;
-            }
-            p.sched = dyn ? d_sched : nullptr;
-            p.sched_base = sched_base;
-            h16.launch(dyn, hi, ho, grid, hi ? smem_h : smem_f32_h, st, m, p);
-            if (dyn)
-                sched_base += static_cast<uint32_t>((p.nbatch + sst::kDrawGroup - 1) / sst::kDrawGroup +
-                                                    grid * (sst::kDrawAhead - 1));
-            ck(cudaGetLastError(), "kernel launch");
-            ++launches;
-            ++h16_launches;
+        const bool hi = t > 0, ho = t + 1 < nsteps;
+        sst::StepParams p = step_params(src);
+        const int grid = grid_size(p);
+        sst::MapSet m{};
+        m.in[0] = m.in[1] = hi ? hin[(t - 1) & 1] : maps.in[src];
+        m.out[0] = m.out[1] = ho ? hout[t & 1] : maps.out[fin];
+        // 3D: the output storage's ring chunks (binary16: the output buffer's own,
+        // converted from buf[src]; fp32: the input buffer's, never rewritten)
+        m.ring[0] = m.ring[1] = ho ? hring[t & 1] : maps.ring[src];
+        float* outp = ho ? reinterpret_cast<float*>(hbuf[t & 1]) : buf[fin];
+        p.src = 0;
+        p.buf[0] = p.buf[1] = outp;
+        p.tmem_cols = tmem_cols_h;
+        if (ho) {
+            p.row_pitch = static_cast<int64_t>(storage_h.row_pitch);
+            p.plane_pitch = static_cast<int64_t>(storage_h.plane_pitch);
+            p.left_pad = static_cast<int32_t>(storage_h.left_pad);
         }
-        return fin;
+        if (hi) {
+            p.load_x0 = load_x0_h;
+            p.patch_w = img_h.geo.patch_w;
+            p.gsrc = d_gsrc_h;
+            p.gdst = d_gdst_h;
+        }
+        const char* dyn_e = std::getenv("SST_DYN");
+        // (the store-only ablation, debug bit 32, has no producer to draw batches)
+        // (the 3D stream kernel splits its work statically)
+        const bool dyn = variant->kz == 0 && !(debug_mode & 32) &&
+                         (dyn_e ? std::atoi(dyn_e) != 0 : p.nbatch >= 8 * grid);
+        if (dyn && !d_sched) {
+            ck(cudaMalloc(&d_sched, 4), "cudaMalloc(sched)");
+            ck(cudaMemsetAsync(d_sched, 0, 4, st), "cudaMemsetAsync(sched)");
+            sched_base = 0;
+        }
+        p.sched = dyn ? d_sched : nullptr;
+        p.sched_base = sched_base;
+        h16.launch(dyn, hi, ho, grid, hi ? smem_h : smem_f32_h, st, m, p);
+        if (dyn)
+            sched_base += static_cast<uint32_t>((p.nbatch + sst::kDrawGroup - 1) / sst::kDrawGroup +
+                                                grid * (sst::kDrawAhead - 1));
+        ck(cudaGetLastError(), "kernel launch");
+        ++launches;
+        ++h16_launches;
+    }
+
+    int launch_h16(int src, uint64_t nsteps, cudaStream_t st) {
+        h16_begin(src, st);
+        for (uint64_t t = 0; t < nsteps; ++t) h16_step(src, t, nsteps, st);
+        return static_cast<int>((static_cast<uint64_t>(src) + nsteps) & 1);
+    }
+
+    // the plan that runs binary16 launches of `nsteps` operator steps, or null when the
+    // run takes the fp32 path (same conditions as launch())
+    sst_plan* h16_runner(uint64_t nsteps) {
+        const char* ms_e = std::getenv("SST_MULTISTEP");
+        const bool ms_env = ms_e && std::atoi(ms_e) != 0;
+        const bool full = !(y_hi > y_lo);
+        const bool multi = ms_env && variant->multistep && full && nsteps > 1 && !fold_n && !peer_buf[0][0] &&
+                           !peer_buf[1][0];
+        sst_plan* hp = typed ? typed.get() : this;
+        if (hp->h16_ok && h16_enabled() && !multi && full && nsteps > 1 && !peer_buf[0][0] && !peer_buf[1][0])
+            return hp;
+        return nullptr;
     }
 
     // streaming kernels: (row-band groups) x nbx CTAs, see stencil3d_kernel.cuh;
@@ -667,13 +689,12 @@ struct sst_plan {
         const bool multi = ms_env && variant->multistep && full && nsteps > 1 && !fold_n && !peer_buf[0][0] &&
                            !peer_buf[1][0];
         const bool mdyn = multi && ms_dyn;
-        if ((typed ? typed->h16_ok : h16_ok) && h16_enabled() && !multi && full && nsteps > 1 && !peer_buf[0][0] &&
-            !peer_buf[1][0]) {
-            if (!typed) return launch_h16(src, nsteps, st);
-            const uint64_t l0 = typed->launches, h0 = typed->h16_launches;
-            const int fin = typed->launch_h16(src, nsteps, st);
-            launches += typed->launches - l0;
-            h16_launches += typed->h16_launches - h0;
+        if (sst_plan* hp = h16_runner(nsteps)) {
+            if (hp == this) return launch_h16(src, nsteps, st);
+            const uint64_t l0 = hp->launches, h0 = hp->h16_launches;
+            const int fin = hp->launch_h16(src, nsteps, st);
+            launches += hp->launches - l0;
+            h16_launches += hp->h16_launches - h0;
             return fin;
         }
         const int grid = grid_size(p, multi && !mdyn);
@@ -1364,6 +1385,58 @@ sst_status sst_run_steps(sst_plan* plan, int src, uint64_t steps, void* stream, 
             throw std::invalid_argument("steps must be a multiple of the fusion factor");
         const int cur = plan->launch(src, steps / plan->fuse, st);
         if (dst_out) *dst_out = cur;
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_run_steps_batch(sst_plan* const* plans, int n, const int* src, uint64_t steps, void* stream,
+                               int* dst_out) {
+    try {
+        if (!plans || n < 1 || !src) throw std::invalid_argument("null argument");
+        for (int i = 0; i < n; ++i) {
+            if (!plans[i]) throw std::invalid_argument("null plan");
+            if (src[i] < 0 || src[i] > 1) throw std::invalid_argument("buffer index must be 0 or 1");
+            if (!plans[i]->tmap_ok) throw std::invalid_argument("plan has no bound buffers");
+            if (plans[i]->device != plans[0]->device) throw std::invalid_argument("plans on different devices");
+            if (plans[i]->fuse != plans[0]->fuse) throw std::invalid_argument("plans with different fusion factors");
+            for (int j = 0; j < i; ++j)
+                if (plans[j] == plans[i]) throw std::invalid_argument("a plan appears twice in the batch");
+        }
+        if (steps % plans[0]->fuse != 0) throw std::invalid_argument("steps must be a multiple of the fusion factor");
+        ck(cudaSetDevice(plans[0]->device), "cudaSetDevice");
+        const auto st = static_cast<cudaStream_t>(stream);
+        const uint64_t L = steps / plans[0]->fuse;
+        std::vector<sst_plan*> hp(static_cast<std::size_t>(n));
+        bool all_h16 = true;
+        for (int i = 0; i < n; ++i) all_h16 &= (hp[static_cast<std::size_t>(i)] = plans[i]->h16_runner(L)) != nullptr;
+        std::vector<int> cur(src, src + n);
+        if (all_h16) {
+            std::vector<uint64_t> l0(static_cast<std::size_t>(n)), h0(static_cast<std::size_t>(n));
+            for (int i = 0; i < n; ++i) {
+                sst_plan* h = hp[static_cast<std::size_t>(i)];
+                l0[static_cast<std::size_t>(i)] = h->launches;
+                h0[static_cast<std::size_t>(i)] = h->h16_launches;
+                h->h16_begin(src[i], st);
+            }
+            for (uint64_t t = 0; t < L; ++t)
+                for (int i = 0; i < n; ++i) hp[static_cast<std::size_t>(i)]->h16_step(src[i], t, L, st);
+            for (int i = 0; i < n; ++i) {
+                sst_plan* h = hp[static_cast<std::size_t>(i)];
+                if (h != plans[i]) {  // companion plan: count on the caller's plan
+                    plans[i]->launches += h->launches - l0[static_cast<std::size_t>(i)];
+                    plans[i]->h16_launches += h->h16_launches - h0[static_cast<std::size_t>(i)];
+                }
+                cur[static_cast<std::size_t>(i)] = static_cast<int>((static_cast<uint64_t>(src[i]) + L) & 1);
+            }
+        } else {
+            for (uint64_t t = 0; t < L; ++t)
+                for (int i = 0; i < n; ++i)
+                    cur[static_cast<std::size_t>(i)] = plans[i]->launch(cur[static_cast<std::size_t>(i)], 1, st);
+        }
+        if (dst_out)
+            for (int i = 0; i < n; ++i) dst_out[i] = cur[static_cast<std::size_t>(i)];
         return SST_OK;
     } catch (...) {
         return sstc::from_current_exception();

@@ -390,3 +390,15 @@ def estimate_device(stencil: str, grid_dims: Sequence[int], fuse: int = 1, stora
     d = dict(zip(keys, list(out)))
     d["bound"] = ("hbm", "smem", "tensor")[int(d["bound"])]
     return d
+
+
+def run_batch(engines: Sequence["SparseStencil"], steps: int, srcs: Optional[Sequence[int]] = None,
+              stream: int = 0) -> list[int]:
+    """sst_run_steps_batch: `steps` time steps of several independent grids (one bound
+    SparseStencil each), launches interleaved step by step; returns each result buffer."""
+    n = len(engines)
+    plans = (C.c_void_p * n)(*[e._h for e in engines])
+    src = (C.c_int * n)(*(srcs if srcs is not None else [0] * n))
+    dst = (C.c_int * n)()
+    check(lib().sst_run_steps_batch(plans, n, src, int(steps), C.c_void_p(stream or None), dst))
+    return list(dst)

@@ -46,7 +46,7 @@ def test_small_grid_line(gpu):
     assert res.returncode == 0, res.stderr[-2000:]
     line = json.loads(res.stdout.strip().splitlines()[-1])
     assert line["gpu_launches"] == 20
-    assert "round-robin" in line["config"]["l2"]
+    assert "stepped together" in line["config"]["l2"]
     roof = line["roofline"]
     assert roof["bound"] == "hbm" and 0.2 < roof["frac"] < 1.3
     assert roof["l2_flushed_single_launch"]["ms_per_launch"] > 0

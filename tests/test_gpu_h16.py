@@ -167,3 +167,56 @@ def test_h16_3d_run_steps_device_buffers(gpu):
         finally:
             os.environ.pop("SST_H16", None)
             eng.close()
+
+
+# ---------------------------------------------------------------- batched runs
+def test_run_batch_equals_individual_runs(gpu):
+    """sst_run_steps_batch: several independent grids (different stencils, 2D and 3D)
+    stepped together, launches interleaved, each bitwise its own sst_run_steps."""
+    import torch
+
+    from paper_2506_22969_b200 import run_batch
+
+    cases = [("Heat-2D", (130, 300)), ("Box-2D9P", (97, 301)), ("Box-3D27P", (20, 24, 70)), ("Heat-2D", (64, 64))]
+    engs, grids = [], []
+    try:
+        for name, dims in cases:
+            e = SparseStencil(name, list(dims))
+            e.bind()
+            engs.append(e)
+            grids.append(torch.from_numpy(oracle.random_grid(dims, seed=len(engs)).astype(np.float32)).cuda())
+        for steps in (1, 2, 7):
+            want = []
+            for e, g in zip(engs, grids):
+                e.upload(g, 0)
+                want.append(e.download(e.run(steps, 0)))
+            for e, g, src in zip(engs, grids, (0, 1, 0, 1)):
+                e.upload(g, src)
+            h0 = [e.stats()["h16_launches"] for e in engs]
+            dst = run_batch(engs, steps, [0, 1, 0, 1])
+            assert dst == [steps & 1, (1 + steps) & 1, steps & 1, (1 + steps) & 1]
+            for e, d, w, h in zip(engs, dst, want, h0):
+                assert np.array_equal(e.download(d).view(np.uint32), w.view(np.uint32))
+                assert e.stats()["h16_launches"] - h == (steps if steps > 1 else 0)
+    finally:
+        for e in engs:
+            e.close()
+
+
+def test_run_batch_rejects_bad_batches(gpu):
+    from paper_2506_22969_b200 import InvalidArgument, run_batch
+
+    e = SparseStencil("Heat-2D", [64, 64])
+    try:
+        e.bind()
+        with pytest.raises(InvalidArgument):
+            run_batch([e, e], 2)
+        f = SparseStencil("Box-2D9P", [64, 64], fuse=2)
+        try:
+            f.bind()
+            with pytest.raises(InvalidArgument):
+                run_batch([e, f], 2)
+        finally:
+            f.close()
+    finally:
+        e.close()
