@@ -65,6 +65,18 @@ for name, owned, rest in (("Box-2D9P", 40, (203,)), ("Box-3D27P", 10, (30, 70)))
         e.download(cur)
         e.close()
     print(name, "p2p slabs done", flush=True)
+# batched binary16 runs (sst_run_steps_batch), 2D + 3D interleaved, ragged edges
+import torch  # noqa: E402
+from paper_2506_22969_b200 import run_batch  # noqa: E402
+bs = [SparseStencil("Heat-2D", [70, 203]), SparseStencil("Heat-3D", [11, 19, 77])]
+for e, d in zip(bs, ([70, 203], [11, 19, 77])):
+    e.bind()
+    e.upload(torch.from_numpy(oracle.random_grid(d, seed=5).astype(np.float32)).cuda(), 0)
+run_batch(bs, 3)
+torch.cuda.synchronize()
+for e in bs:
+    e.close()
+print("batch done", flush=True)
 os.environ["SST_MULTISTEP"] = "1"
 eng = SparseStencil("Box-2D9P", [200, 300])
 eng.apply_host(oracle.random_grid((200, 300), seed=2).astype(np.float32), 5)
