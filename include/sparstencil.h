@@ -202,6 +202,13 @@ SST_API sst_status sst_plan_set_peer(sst_plan* plan, int which, void* buf0, void
 /* The plan's own ping-pong allocations (after sst_plan_bind(plan, NULL, NULL)):
  * what sst_plan_set_peer expects of a neighbour (and what to export by IPC). */
 SST_API sst_status sst_plan_buffers(const sst_plan* plan, void** buf0, void** buf1);
+/* Binary16 inter-step storage of a slab (3D): the plan's own binary16 ping-pong pair
+ * (what a neighbour registers with sst_plan_set_peer_h; export by IPC like the fp32
+ * pair), and the neighbour's pair, registered after its fp32 pair (sst_plan_set_peer).
+ * With both registered for every neighbour, runs of >= 2 steps keep binary16 between
+ * steps, halos included (bitwise the fp32-storage result); else they stay fp32. */
+SST_API sst_status sst_plan_buffers_h(sst_plan* plan, void** h0, void** h1);
+SST_API sst_status sst_plan_set_peer_h(sst_plan* plan, int which, void* h0, void* h1);
 /* Zero-initialised device allocation (IPC-exportable, unlike sub-allocations). */
 SST_API sst_status sst_device_alloc(int device, size_t bytes, void** ptr);
 SST_API sst_status sst_device_free(void* ptr);

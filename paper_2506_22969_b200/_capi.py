@@ -29,7 +29,7 @@ EXPORTED = [
     "sst_ipc_open", "sst_ipc_close", "sst_stream_write_u32", "sst_stream_wait_geq_u32",
     "sst_run_steps_peer", "sst_download_slices", "sst_multi_create", "sst_multi_destroy", "sst_multi_upload",
     "sst_multi_run", "sst_multi_sync", "sst_multi_download", "sst_multi_slab", "sst_run_steps_multi",
-    "sst_estimate_device", "sst_run_steps_batch",
+    "sst_estimate_device", "sst_run_steps_batch", "sst_plan_buffers_h", "sst_plan_set_peer_h",
 ]
 
 
@@ -160,6 +160,8 @@ def lib() -> C.CDLL:
         "sst_run_steps_batch": (i32, [C.POINTER(P), i32, C.POINTER(i32), u64, P, C.POINTER(i32)]),
         "sst_plan_set_peer": (i32, [P, i32, P, P, u64]),
         "sst_plan_buffers": (i32, [P, C.POINTER(P), C.POINTER(P)]),
+        "sst_plan_buffers_h": (i32, [P, C.POINTER(P), C.POINTER(P)]),
+        "sst_plan_set_peer_h": (i32, [P, i32, P, P]),
         "sst_device_alloc": (i32, [i32, sz, C.POINTER(P)]),
         "sst_device_free": (i32, [P]),
         "sst_ipc_handle": (i32, [P, C.POINTER(C.c_uint8)]),

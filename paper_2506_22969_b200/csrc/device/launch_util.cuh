@@ -107,9 +107,10 @@ std::vector<TypedFns> typed_fns_3d(int tyb, int np, int kz, bool a_tmem, int nb,
 
 // Boundary ring (and everything outside the interior the kernels read) of an f32
 // storage buffer -> binary16 in two f16 storage buffers (runtime.cu).
+// halo_lo / halo_hi: 3D slab ends whose r planes a P2P neighbour writes (ring cells only)
 void launch_ring_to_half(const float* src, __half* d0, __half* d1, int gx, int gy, int gz, int r,
                          long long rp, long long pp, int lp, long long rph, long long pph, int lph,
-                         cudaStream_t st);
+                         cudaStream_t st, bool halo_lo = false, bool halo_hi = false);
 
 // Stream-ordered flag write / wait >= (cuStreamWriteValue32 / cuStreamWaitValue32,
 // resolved at run time through the driver entry points; runtime.cu).

@@ -152,20 +152,20 @@ sst_status sst_multi_create(const sst_plan_desc* global, int nslabs, const int* 
                     ck(e, "cudaDeviceEnablePeerAccess");
             }
         }
+        // binary16 pairs too (3D f16 plans), so runs keep binary16 between steps
+        const bool h16 = global->dims == 3 && global->precision == SST_PREC_F16;
+        auto wire = [&](Slab& s, int which, const Slab& nb) {
+            void *b0 = nullptr, *b1 = nullptr;
+            check(sst_plan_buffers(nb.plan, &b0, &b1));
+            check(sst_plan_set_peer(s.plan, which, b0, b1, nb.hi - nb.lo));
+            void *h0 = nullptr, *h1 = nullptr;
+            if (h16 && sst_plan_buffers_h(nb.plan, &h0, &h1) == SST_OK)
+                check(sst_plan_set_peer_h(s.plan, which, h0, h1));
+        };
         for (std::size_t i = 0; i < M->slabs.size(); ++i) {
             auto& s = M->slabs[i];
-            if (i > 0) {
-                const auto& u = M->slabs[i - 1];
-                void *b0 = nullptr, *b1 = nullptr;
-                check(sst_plan_buffers(u.plan, &b0, &b1));
-                check(sst_plan_set_peer(s.plan, 0, b0, b1, u.hi - u.lo));
-            }
-            if (i + 1 < M->slabs.size()) {
-                const auto& w = M->slabs[i + 1];
-                void *b0 = nullptr, *b1 = nullptr;
-                check(sst_plan_buffers(w.plan, &b0, &b1));
-                check(sst_plan_set_peer(s.plan, 1, b0, b1, w.hi - w.lo));
-            }
+            if (i > 0) wire(s, 0, M->slabs[i - 1]);
+            if (i + 1 < M->slabs.size()) wire(s, 1, M->slabs[i + 1]);
         }
         *out = M.release();
         return SST_OK;
@@ -197,7 +197,41 @@ sst_status sst_multi_run(sst_multi* m, uint64_t steps) {
         if (!m) throw std::invalid_argument("null argument");
         if (steps % m->fuse != 0) throw std::invalid_argument("steps must be a multiple of the fusion factor");
         const std::size_t n = m->slabs.size();
-        for (uint64_t t = 0; t < steps / m->fuse; ++t) {
+        const uint64_t L = steps / m->fuse;
+        // binary16 between steps when every slab's run qualifies (sstc::plan_h16_runner)
+        std::vector<sst_plan*> hp(n, nullptr);
+        bool h16 = L > 1;
+        for (std::size_t i = 0; i < n && h16; ++i) h16 = (hp[i] = sstc::plan_h16_runner(m->slabs[i].plan, L)) != nullptr;
+        if (h16) {
+            std::vector<uint64_t> l0(n), h0(n);
+            for (std::size_t i = 0; i < n; ++i) {
+                auto& s = m->slabs[i];
+                ck(cudaSetDevice(s.device), "cudaSetDevice");
+                l0[i] = sstc::plan_launches(hp[i], false);
+                h0[i] = sstc::plan_launches(hp[i], true);
+                sstc::plan_h16_begin(hp[i], m->cur, s.stream);
+            }
+            for (uint64_t t = 0; t < L; ++t) {
+                const uint32_t u = m->launches;
+                for (std::size_t i = 0; i < n; ++i) {
+                    auto& s = m->slabs[i];
+                    ck(cudaSetDevice(s.device), "cudaSetDevice");
+                    if (i > 0) sstl::stream_wait_geq(s.stream, s.flags + 0, u);
+                    if (i + 1 < n) sstl::stream_wait_geq(s.stream, s.flags + 1, u);
+                    sstc::plan_h16_step(hp[i], m->cur, t, L, s.stream);
+                    if (i > 0) sstl::stream_write(s.stream, m->slabs[i - 1].flags + 1, u + 1);
+                    if (i + 1 < n) sstl::stream_write(s.stream, m->slabs[i + 1].flags + 0, u + 1);
+                }
+                m->launches = u + 1;
+            }
+            for (std::size_t i = 0; i < n; ++i)
+                if (hp[i] != m->slabs[i].plan)
+                    sstc::plan_add_launches(m->slabs[i].plan, sstc::plan_launches(hp[i], false) - l0[i],
+                                            sstc::plan_launches(hp[i], true) - h0[i]);
+            m->cur = static_cast<int>((static_cast<uint64_t>(m->cur) + L) & 1);
+            return SST_OK;
+        }
+        for (uint64_t t = 0; t < L; ++t) {
             const uint32_t u = m->launches;
             int dst = m->cur;
             for (std::size_t i = 0; i < n; ++i) {

@@ -185,13 +185,21 @@ namespace {
 // the whole ring planes — then the r left + r right cells of every other row). A
 // warp-per-row loop serialised the full ring rows behind the possible aliasing of its
 // loads and stores (8192-cell rows: 114 us per run; this: a few us).
+// 3D slabs (halo_lo / halo_hi): the r planes at that z end are a neighbour's interior,
+// written by its epilogue every step: only their x / y ring cells are converted
+// (as for an interior plane), never their interior, which the neighbour may already
+// have stored for this run.
 __global__ void ring_to_half_kernel(const float* __restrict__ src, __half* __restrict__ d0,
                                     __half* __restrict__ d1, int gx, int gy, int gz, int r, long long rp,
-                                    long long pp, int lp, long long rph, long long pph, int lph) {
+                                    long long pp, int lp, long long rph, long long pph, int lph, int halo_lo,
+                                    int halo_hi) {
     const bool d3 = gz > 1;
-    const long long full_planes_rows = d3 ? 2LL * r * gy : 0;                // rows of the z ring planes
-    const long long full_rows = full_planes_rows + 2LL * r * (d3 ? gz - 2 * r : 1);  // + y ring rows
-    const long long inner_rows = static_cast<long long>(gy - 2 * r) * (d3 ? gz - 2 * r : 1);
+    // z planes converted whole: [0, zl) and [gz - zh, gz); the others [zl, gz - zh) like interior planes
+    const int zl = d3 && !halo_lo ? r : 0, zh = d3 && !halo_hi ? r : 0;
+    const int nin = d3 ? gz - zl - zh : 1;  // planes converted ring-only
+    const long long full_planes_rows = static_cast<long long>(zl + zh) * gy;  // rows of the whole planes
+    const long long full_rows = full_planes_rows + 2LL * r * nin;            // + y ring rows
+    const long long inner_rows = static_cast<long long>(gy - 2 * r) * nin;
     const long long n_full = full_rows * gx, n_all = n_full + inner_rows * 2 * r;
     for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_all;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -202,11 +210,11 @@ __global__ void ring_to_half_kernel(const float* __restrict__ src, __half* __res
             if (f < full_planes_rows) {
                 const int pz = static_cast<int>(f / gy);
                 y = static_cast<int>(f % gy);
-                z = pz < r ? pz : gz - 2 * r + pz;
+                z = pz < zl ? pz : gz - zh - zl + pz;
             } else {
                 const long long g = f - full_planes_rows;
                 const int j = static_cast<int>(g % (2 * r));
-                z = d3 ? r + static_cast<int>(g / (2 * r)) : 0;
+                z = d3 ? zl + static_cast<int>(g / (2 * r)) : 0;
                 y = j < r ? j : gy - 2 * r + j;
             }
         } else {
@@ -215,7 +223,7 @@ __global__ void ring_to_half_kernel(const float* __restrict__ src, __half* __res
             const int j = static_cast<int>(g % (2 * r));
             x = j < r ? j : gx - 2 * r + j;
             y = r + static_cast<int>(row % (gy - 2 * r));
-            z = d3 ? r + static_cast<int>(row / (gy - 2 * r)) : 0;
+            z = d3 ? zl + static_cast<int>(row / (gy - 2 * r)) : 0;
         }
         const __half h = __float2half_rn(src[z * pp + y * rp + lp + x]);
         const long long o = z * pph + y * rph + lph + x;
@@ -226,9 +234,11 @@ __global__ void ring_to_half_kernel(const float* __restrict__ src, __half* __res
 }  // namespace
 
 void sstl::launch_ring_to_half(const float* src, __half* d0, __half* d1, int gx, int gy, int gz, int r, long long rp,
-                               long long pp, int lp, long long rph, long long pph, int lph, cudaStream_t st) {
+                               long long pp, int lp, long long rph, long long pph, int lph, cudaStream_t st,
+                               bool halo_lo, bool halo_hi) {
     if (r == 0) return;
-    ring_to_half_kernel<<<148 * 8, 256, 0, st>>>(src, d0, d1, gx, gy, gz, r, rp, pp, lp, rph, pph, lph);
+    ring_to_half_kernel<<<148 * 8, 256, 0, st>>>(src, d0, d1, gx, gy, gz, r, rp, pp, lp, rph, pph, lph,
+                                                 halo_lo ? 1 : 0, halo_hi ? 1 : 0);
 }
 
 struct sst_plan {
@@ -296,6 +306,12 @@ struct sst_plan {
     __half* hbuf[2] = {nullptr, nullptr};
     CUtensorMap hin[2]{}, hout[2]{};  // f16 patch loads / interior stores
     CUtensorMap hring[2]{};           // 3D: the f16 buffers' right-edge ring chunks (kEdgeRing)
+    // 3D slabs with P2P halos in binary16 runs: the neighbours' binary16 buffers
+    // (sst_plan_set_peer_h) and, per launch kind, the PeerMaps the kernel reads at
+    // [p.src ^ 1] = [1]: {f16 out hbuf[0], f16 out hbuf[1], fp32 out buf[0], fp32 out buf[1]}
+    __half* peer_hbuf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    sst::PeerMaps* d_peer_maps_run = nullptr;
+    bool run_maps_ok = false;
     bool hmaps_ok = false;
     uint64_t h16_launches = 0;        // launches that read or wrote binary16 storage
     int variant_index = -1;
@@ -316,6 +332,7 @@ struct sst_plan {
         cudaFree(d_sched);
         cudaFree(d_ring_save);
         cudaFree(d_peer_maps);
+        cudaFree(d_peer_maps_run);
         cudaFree(d_gsrc_h);
         cudaFree(d_gdst_h);
         cudaFree(hbuf[0]);
@@ -583,8 +600,34 @@ struct sst_plan {
                                   static_cast<long long>(storage.row_pitch), static_cast<long long>(storage.plane_pitch),
                                   static_cast<int>(storage.left_pad), static_cast<long long>(storage_h.row_pitch),
                                   static_cast<long long>(storage_h.plane_pitch), static_cast<int>(storage_h.left_pad),
-                                  st);
+                                  st, peer_buf[0][0] != nullptr, peer_buf[1][0] != nullptr);
         ck(cudaGetLastError(), "ring_to_half launch");
+        if ((peer_buf[0][0] || peer_buf[1][0]) && !run_maps_ok) make_run_peer_maps();
+    }
+
+    // the PeerMaps of binary16 slab runs (see d_peer_maps_run)
+    void make_run_peer_maps() {
+        sst::PeerMaps pm[4]{};
+        const cuuint64_t gstride[2] = {storage_h.row_pitch * 2, storage_h.plane_pitch * 2};
+        const int ox = gx - 2 * r, ox8 = ox & ~7, oxs = (ox & 7) ? ox8 + 8 : ox8;
+        const cuuint32_t obox[3] = {64u, static_cast<cuuint32_t>(tiles_y * sst::kTileH), 1u};
+        const int64_t inner0 = static_cast<int64_t>(r) * static_cast<int64_t>(storage_h.row_pitch) +
+                               static_cast<int64_t>(storage_h.left_pad) + r;
+        for (int w = 0; w < 2; ++w) {
+            if (!peer_buf[w][0]) continue;
+            const int64_t first = w == 0 ? static_cast<int64_t>(peer_slices[0]) - r : 0;
+            for (int i = 0; i < 2; ++i) {
+                __half* base = peer_hbuf[w][i] + first * static_cast<int64_t>(storage_h.plane_pitch) + inner0;
+                const cuuint64_t pdim[3] = {static_cast<cuuint64_t>(std::max(oxs, 8)),
+                                            static_cast<cuuint64_t>(gy - 2 * r), static_cast<cuuint64_t>(r)};
+                encode(w == 0 ? &pm[i].up[1] : &pm[i].down[1], 3, base, pdim, gstride, obox,
+                       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+                (w == 0 ? pm[2 + i].up[1] : pm[2 + i].down[1]) = w == 0 ? peer_maps_h.up[i] : peer_maps_h.down[i];
+            }
+        }
+        if (!d_peer_maps_run) ck(cudaMalloc(&d_peer_maps_run, sizeof pm), "cudaMalloc(run peer maps)");
+        ck(cudaMemcpy(d_peer_maps_run, pm, sizeof pm, cudaMemcpyHostToDevice), "cudaMemcpy(run peer maps)");
+        run_maps_ok = true;
     }
 
     void h16_step(int src, uint64_t t, uint64_t nsteps, cudaStream_t st) {
@@ -625,6 +668,7 @@ struct sst_plan {
         }
         p.sched = dyn ? d_sched : nullptr;
         p.sched_base = sched_base;
+        if (p.peer_mask) p.peer_maps = d_peer_maps_run + (ho ? static_cast<int>(t & 1) : 2 + fin);
         h16.launch(dyn, hi, ho, grid, hi ? smem_h : smem_f32_h, st, m, p);
         if (dyn)
             sched_base += static_cast<uint32_t>((p.nbatch + sst::kDrawGroup - 1) / sst::kDrawGroup +
@@ -649,8 +693,11 @@ struct sst_plan {
         const bool multi = ms_env && variant->multistep && full && nsteps > 1 && !fold_n && !peer_buf[0][0] &&
                            !peer_buf[1][0];
         sst_plan* hp = typed ? typed.get() : this;
-        if (hp->h16_ok && h16_enabled() && !multi && full && nsteps > 1 && !peer_buf[0][0] && !peer_buf[1][0])
-            return hp;
+        // slab peers: 3D only, and every fp32 peer must have its binary16 buffers too
+        bool peers_ok = true;
+        for (int w = 0; w < 2; ++w)
+            if (peer_buf[w][0]) peers_ok &= dims == 3 && hp->peer_buf[w][0] && hp->peer_hbuf[w][0];
+        if (hp->h16_ok && h16_enabled() && !multi && full && nsteps > 1 && peers_ok) return hp;
         return nullptr;
     }
 
@@ -1228,6 +1275,17 @@ sst_status sst_plan_set_peer(sst_plan* plan, int which, void* buf0, void* buf1, 
         plan->peer_buf[which][1] = buf1 ? static_cast<float*>(buf1) + plan->guard_elems() : nullptr;
         plan->peer_slices[which] = buf0 ? peer_slices : 0;
         if (plan->tmap_ok) plan->make_tmaps();
+        plan->run_maps_ok = false;
+        if (!buf0) plan->peer_hbuf[which][0] = plan->peer_hbuf[which][1] = nullptr;
+        if (plan->typed) {  // the companion plan runs the binary16 launches of the same slab
+            sst_plan* T = plan->typed.get();
+            T->peer_buf[which][0] = plan->peer_buf[which][0];
+            T->peer_buf[which][1] = plan->peer_buf[which][1];
+            T->peer_slices[which] = plan->peer_slices[which];
+            if (T->tmap_ok) T->make_tmaps();
+            T->run_maps_ok = false;
+            if (!buf0) T->peer_hbuf[which][0] = T->peer_hbuf[which][1] = nullptr;
+        }
         return SST_OK;
     } catch (...) {
         return sstc::from_current_exception();
@@ -1240,6 +1298,37 @@ sst_status sst_plan_buffers(const sst_plan* plan, void** buf0, void** buf1) {
         if (!plan->owns_buf) throw std::invalid_argument("plan buffers are caller-owned");
         *buf0 = plan->alloc_base[0];
         *buf1 = plan->alloc_base[1];
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_plan_buffers_h(sst_plan* plan, void** h0, void** h1) {
+    try {
+        if (!plan || !h0 || !h1) throw std::invalid_argument("null argument");
+        sst_plan* hp = plan->typed ? plan->typed.get() : plan;
+        if (!hp->h16_ok) throw std::invalid_argument("plan has no binary16 storage");
+        ck(cudaSetDevice(hp->device), "cudaSetDevice");
+        hp->ensure_h16();
+        *h0 = hp->hbuf[0];
+        *h1 = hp->hbuf[1];
+        return SST_OK;
+    } catch (...) {
+        return sstc::from_current_exception();
+    }
+}
+
+sst_status sst_plan_set_peer_h(sst_plan* plan, int which, void* h0, void* h1) {
+    try {
+        if (!plan) throw std::invalid_argument("null plan");
+        if (which != 0 && which != 1) throw std::invalid_argument("peer must be 0 (upper) or 1 (lower)");
+        if ((h0 == nullptr) != (h1 == nullptr)) throw std::invalid_argument("peer needs both buffers");
+        if (h0 && !plan->peer_buf[which][0]) throw std::invalid_argument("set the fp32 peer (sst_plan_set_peer) first");
+        sst_plan* hp = plan->typed ? plan->typed.get() : plan;
+        hp->peer_hbuf[which][0] = static_cast<__half*>(h0);
+        hp->peer_hbuf[which][1] = static_cast<__half*>(h1);
+        hp->run_maps_ok = false;
         return SST_OK;
     } catch (...) {
         return sstc::from_current_exception();
@@ -1391,6 +1480,24 @@ sst_status sst_run_steps(sst_plan* plan, int src, uint64_t steps, void* stream, 
     }
 }
 
+}  // extern "C"
+
+// binary16 runs of slab plans for the in-process multi-slab driver (multi.cu)
+namespace sstc {
+sst_plan* plan_h16_runner(sst_plan* p, uint64_t launches) { return p->h16_runner(launches); }
+void plan_h16_begin(sst_plan* hp, int src, void* st) { hp->h16_begin(src, static_cast<cudaStream_t>(st)); }
+void plan_h16_step(sst_plan* hp, int src, uint64_t t, uint64_t launches, void* st) {
+    hp->h16_step(src, t, launches, static_cast<cudaStream_t>(st));
+}
+uint64_t plan_launches(const sst_plan* p, bool h16) { return h16 ? p->h16_launches : p->launches; }
+void plan_add_launches(sst_plan* p, uint64_t launches, uint64_t h16) {
+    p->launches += launches;
+    p->h16_launches += h16;
+}
+}  // namespace sstc
+
+extern "C" {
+
 sst_status sst_run_steps_batch(sst_plan* const* plans, int n, const int* src, uint64_t steps, void* stream,
                                int* dst_out) {
     try {
@@ -1457,6 +1564,24 @@ sst_status sst_run_steps_peer(sst_plan* plan, int src, uint64_t steps, void* str
         const auto st = static_cast<cudaStream_t>(stream);
         int cur = src;
         const uint64_t launches = steps / plan->fuse;
+        if (sst_plan* hp = plan->h16_runner(launches)) {  // binary16 between steps (3D slabs)
+            const uint64_t l0 = hp->launches, h0 = hp->h16_launches;
+            hp->h16_begin(src, st);
+            for (uint64_t i = 0; i < launches; ++i) {
+                const uint32_t u = launch0 + static_cast<uint32_t>(i);
+                if (up) sstl::stream_wait_geq(st, my_flags + 0, u);
+                if (down) sstl::stream_wait_geq(st, my_flags + 1, u);
+                hp->h16_step(src, i, launches, st);
+                if (up) sstl::stream_write(st, up_flag, u + 1);
+                if (down) sstl::stream_write(st, down_flag, u + 1);
+            }
+            if (hp != plan) {
+                plan->launches += hp->launches - l0;
+                plan->h16_launches += hp->h16_launches - h0;
+            }
+            if (dst_out) *dst_out = static_cast<int>((static_cast<uint64_t>(src) + launches) & 1);
+            return SST_OK;
+        }
         for (uint64_t i = 0; i < launches; ++i) {
             const uint32_t u = launch0 + static_cast<uint32_t>(i);
             // both neighbours finished launch u - 1: this launch's input halos are in

@@ -95,7 +95,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     static_assert(NACC > KZ, "one accumulator beyond the KZ open ones");
     static_assert(N % 16 == 0 && N <= 128, "UMMA N for M=128");
     static_assert(NACC * N <= 320, "accumulator ring must leave TMEM room for metadata / A''");
-    static_assert(!(PEER && (HIN || HOUT)), "slab peers use fp32 storage");
     constexpr int ELEM = HIN ? 2 : 4;   // patch element bytes
     constexpr int RW = HOUT ? 8 : 4;    // cells per 16-byte output chunk (ring cache row)
     using namespace ptx;
@@ -333,10 +332,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 if constexpr (HOUT) {
                     if (!(p.debug_mode & 1))
-                        store_batch_h<3, TYB, NS, kEdgeRing>(p, tmap_out,
-                                                             reinterpret_cast<__half*>(buf_of(p, p.src ^ 1)), v, sS,
-                                                             L.s_stride, o, X0, Y0, p.slow_lo + zo, q, lane, etid,
-                                                             reinterpret_cast<const __half*>(ring));
+                        store_batch_h<3, TYB, NS, kEdgeRing>(
+                            p, tmap_out, reinterpret_cast<__half*>(buf_of(p, p.src ^ 1)), v, sS, L.s_stride, o, X0,
+                            Y0, p.slow_lo + zo, q, lane, etid, reinterpret_cast<const __half*>(ring),
+                            (PEER && (p.peer_mask & 1)) ? &p.peer_maps->up[p.src ^ 1] : nullptr,
+                            (PEER && (p.peer_mask & 2)) ? &p.peer_maps->down[p.src ^ 1] : nullptr);
                 } else if (!(p.debug_mode & 1))
                     store_batch<3, TYB, NS, kEdgeRing, PEER>(
                         p, tmap_out, buf_of(p, p.src ^ 1), v, sS, L.s_stride, o, X0, Y0, p.slow_lo + zo, q, lane,

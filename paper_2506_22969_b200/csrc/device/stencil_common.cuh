@@ -547,11 +547,15 @@ __device__ __forceinline__ void store_right_edge_h(const StepParams& p, __half* 
 // map runs to ox8 + 8 and the cells [ox, ox8 + 8) of that last 16-byte chunk are
 // staged with the output storage's own (constant) binary16 values from `ring`
 // (TYB*8 rows x 8 halves).
+// peer_up / peer_down (3D slabs with P2P halos): the neighbours' binary16 halo
+// planes, stored from the same staged boxes as in store_batch.
 template <int DIMS, int TYB, int NS, int EDGE = kEdgePlain>
 __device__ __forceinline__ void store_batch_h(const StepParams& p, const CUtensorMap* tmap_out, __half* dst,
                                               uint32_t (&v)[kTXB / 2][2 * TYB], uint8_t* sS,
                                               uint32_t s_stride, int nb, int X0, int Y0, int Z0, uint32_t q,
-                                              uint32_t lane, int etid, const __half* ring = nullptr) {
+                                              uint32_t lane, int etid, const __half* ring = nullptr,
+                                              const CUtensorMap* peer_up = nullptr,
+                                              const CUtensorMap* peer_down = nullptr) {
     using namespace ptx;
     constexpr int CW = 2 * TYB, NBOX = kTXB / 2;
     constexpr int HBOX = 64;  // halves per 128-byte box row
@@ -608,6 +612,24 @@ __device__ __forceinline__ void store_batch_h(const StepParams& p, const CUtenso
                 tma_store_2d(tmap_out, sS + buf + cb * s_stride, bx0, Y0 - p.slow_lo);
             else
                 tma_store_3d(tmap_out, sS + buf + cb * s_stride, bx0, Y0, Z0);
+        }
+        if constexpr (DIMS == 3) {
+            if (peer_up != nullptr && Z0 < p.r) {
+#pragma unroll 1
+                for (int cb = 0; cb < NBOX / 2; ++cb) {
+                    const int bx0 = X0 + cb * HBOX;
+                    if (bx0 >= oxs) break;
+                    tma_store_3d(peer_up, sS + buf + cb * s_stride, bx0, Y0, Z0);
+                }
+            }
+            if (peer_down != nullptr && Z0 + 1 > p.peer_down0) {
+#pragma unroll 1
+                for (int cb = 0; cb < NBOX / 2; ++cb) {
+                    const int bx0 = X0 + cb * HBOX;
+                    if (bx0 >= oxs) break;
+                    tma_store_3d(peer_down, sS + buf + cb * s_stride, bx0, Y0, Z0 - p.peer_down_c0);
+                }
+            }
         }
         bulk_commit();
     }

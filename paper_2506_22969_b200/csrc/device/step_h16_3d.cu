@@ -18,9 +18,10 @@ namespace {
 // NP32 / NP16: patch ring depth of the kernels reading fp32 / binary16 patches
 template <int TYB, int NP32, int NP16, int KZ, bool AT, int NB, int NACC, int NS>
 struct Typed3D {
-    template <bool HI, bool HO>
+    // PR: the slab P2P halo stores (launched when peers are registered)
+    template <bool HI, bool HO, bool PR = false>
     static KernelFn k() {
-        return sst::stencil3d_stream_kernel<TYB, HI ? NP16 : NP32, KZ, NB, NACC, NS, AT, false, HI, HO>;
+        return sst::stencil3d_stream_kernel<TYB, HI ? NP16 : NP32, KZ, NB, NACC, NS, AT, PR, HI, HO>;
     }
     static int smem(bool hin, int nks, int k_pad, int pw, int ph, int) {
         const sst::SmemLayout L =
@@ -32,11 +33,16 @@ struct Typed3D {
         raise_smem_attr(k<false, true>(), smem32);
         raise_smem_attr(k<true, true>(), smem16);
         raise_smem_attr(k<true, false>(), smem16);
+        raise_smem_attr(k<false, true, true>(), smem32);
+        raise_smem_attr(k<true, true, true>(), smem16);
+        raise_smem_attr(k<true, false, true>(), smem16);
     }
     static void launch(bool, bool hin, bool hout, int grid, int smem, cudaStream_t st, const sst::MapSet& maps,
                        const sst::StepParams& p) {
         if (!hin && !hout) throw std::logic_error("typed launch without binary16 storage");
-        const KernelFn f = hin ? (hout ? k<true, true>() : k<true, false>()) : k<false, true>();
+        const KernelFn f = p.peer_mask ? (hin ? (hout ? k<true, true, true>() : k<true, false, true>())
+                                              : k<false, true, true>())
+                                       : (hin ? (hout ? k<true, true>() : k<true, false>()) : k<false, true>());
         launch_pdl(f, grid, smem, st, maps, p, false);
     }
     static TypedFns fns() {

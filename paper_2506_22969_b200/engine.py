@@ -218,7 +218,7 @@ class MultiSlabStencil:
         s = _capi.PlanStats()
         check(lib().sst_plan_stats_get(plan, C.byref(s)))
         return {"owned": (owned[0], owned[1]), "stream": stream.value, "plan": plan.value,
-                "launches": int(s.launches)}
+                "launches": int(s.launches), "h16_launches": int(s.h16_launches)}
 
     def upload(self, grid):
         on_dev, ptr, keep = _pointer(grid)

@@ -160,6 +160,7 @@ class SlabStencil:
         if halo not in ("nccl", "p2p"):
             raise ValueError("halo must be 'nccl' or 'p2p'")
         self.halo = halo
+        self.precision = precision
         import torch
 
         from .engine import Compiled, SparseStencil
@@ -211,8 +212,15 @@ class SlabStencil:
             check(L.sst_ipc_handle(C.c_void_p(ptr), h))
             return bytes(h)
 
+        # 3D f16 plans also export their binary16 pair: runs then keep binary16 between
+        # steps, halos included (sst_plan_set_peer_h)
+        hbufs = None
+        if len(self.local_dims) == 3 and self.precision == "f16":
+            h0, h1 = C.c_void_p(), C.c_void_p()
+            if L.sst_plan_buffers_h(self.eng._h, C.byref(h0), C.byref(h1)) == 0:
+                hbufs = [handle(h0.value), handle(h1.value)]
         mine = {"bufs": [handle(b0.value), handle(b1.value)], "flags": handle(flags.value),
-                "slices": self.layout.local_slices, "device": int(self.device)}
+                "slices": self.layout.local_slices, "device": int(self.device), "hbufs": hbufs}
         table = [None] * self.layout.world
         dist.all_gather_object(table, mine, group=self.group)
 
@@ -238,6 +246,9 @@ class SlabStencil:
             pb = [open_(e["bufs"][0]), open_(e["bufs"][1])]
             check(L.sst_plan_set_peer(self.eng._h, which, C.c_void_p(pb[0]), C.c_void_p(pb[1]),
                                       int(e["slices"])))
+            if hbufs is not None and e.get("hbufs"):
+                ph = [open_(e["hbufs"][0]), open_(e["hbufs"][1])]
+                check(L.sst_plan_set_peer_h(self.eng._h, which, C.c_void_p(ph[0]), C.c_void_p(ph[1])))
             # my step count goes into the neighbour's slot that names me: I am the
             # lower neighbour (from_down, +4) of my upper one and vice versa
             self._peer_flag[which] = open_(e["flags"]) + (4 if which == 0 else 0)

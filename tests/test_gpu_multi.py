@@ -98,3 +98,23 @@ def test_explorer_choice_runs_on_the_device(gpu, name, dims):
         eng.close()
     assert np.array_equal(out[(slice(1, -1),) * len(dims)].astype(np.float64),
                           oracle.direct_apply(name, g.astype(np.float64), 1))
+
+
+@pytest.mark.parametrize("name,dims,nslabs", [("Box-3D27P", (40, 36, 70), 3), ("Heat-3D", (33, 17, 129), 2),
+                                              ("Box-3D27P", (24, 40, 133), 4)])
+def test_multi_3d_binary16_halos(gpu, name, dims, nslabs):
+    """3D slabs keep binary16 between steps, halos included (the neighbours' binary16
+    pairs registered with sst_plan_set_peer_h): bitwise the single-domain sweep, every
+    launch a binary16 one, across repeated runs."""
+    g = oracle.random_grid(dims, seed=31).astype(np.float32)
+    m = MultiSlabStencil(name, list(dims), [0] * nslabs)
+    try:
+        m.upload(g)
+        m.run(5)
+        m.run(3)
+        got = m.download()
+        st = [m.slab(i) for i in range(nslabs)]
+    finally:
+        m.close()
+    assert np.array_equal(got.view(np.uint32), single(name, g, 8).view(np.uint32))
+    assert all(s["launches"] == 8 and s["h16_launches"] == 8 for s in st), st

@@ -33,7 +33,7 @@ def _rank(rank, world, port, name, owned, rest, steps, fuse, q, halo="nccl"):
         torch.cuda.synchronize()
         out = eng.result()
         a, b = lay.computed()
-        q.put((rank, lay.lo + a, out[a:b], eng.launches()))
+        q.put((rank, lay.lo + a, out[a:b], eng.launches(), int(eng.eng.stats()["h16_launches"])))
         eng.close()
         dist.barrier()
     finally:
@@ -81,10 +81,12 @@ def test_two_ranks_equal_single_domain(gpu, tmp_path, name, owned, rest, steps, 
     ref = SparseStencil(name, dims, fuse=fuse)
     full = ref.apply_host(glob, steps)
     ref.close()
-    for rank, g0, rows, launches in parts:
+    for rank, g0, rows, launches, h16 in parts:
         assert np.array_equal(rows, full[g0:g0 + len(rows)]), (rank, np.abs(rows - full[g0:g0 + len(rows)]).max())
         # nccl: interior window + one boundary window per step; p2p: one launch per step
         assert launches == (steps // fuse) * (2 if halo == "nccl" else 1)
+        # 3D p2p slabs keep binary16 between steps, halos included (IPC-mapped binary16 pairs)
+        assert h16 == (steps // fuse if (halo == "p2p" and len(rest) == 2) else 0)
 
 
 @pytest.mark.parametrize("name,owned,rest,steps", [("Box-2D9P", 100, (203,), 5), ("Box-3D27P", 16, (30, 70), 4),
