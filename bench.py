@@ -496,9 +496,17 @@ def run_engine(args, cfg, cfg_name):
         from paper_2506_22969_b200 import estimate_device
 
         m = estimate_device(stencil, dims, fuse=args.fuse, storage=2 if h16_launches else 4)
+        # the shared-memory pipe as a second roofline: the model's wavefronts per launch
+        # (one 128-byte wavefront per SM clock at peak) over the measured launch time
+        sm_clk = 148 * (clk.get("sm_mhz") or 1965.0) * 1e6
         line["roofline"]["model"] = {"predicted_ms_per_launch": m["t_total"] * 1e3, "bound": m["bound"],
                                      "t_hbm_ms": m["t_hbm"] * 1e3, "t_smem_ms": m["t_smem"] * 1e3,
-                                     "t_tensor_ms": m["t_mma"] * 1e3}
+                                     "t_tensor_ms": m["t_mma"] * 1e3,
+                                     "smem_wavefronts_per_launch": m["smem_wavefronts"],
+                                     "smem_pipe_frac": m["smem_wavefronts"] / (t_kernel * sm_clk),
+                                     "note": "estimate_device (hwmodel.hpp): smem_pipe_frac = modelled shared-memory "
+                                             "wavefronts / (launch time x 148 SMs x SM clock); ncu l1tex throughput "
+                                             "73-90 % (profiles/round2/ncu_*_full.txt)"}
     except Exception:
         pass
     if ws == 1 and not args.no_sweep and args.fuse == 1 and args.precision == "f16":
