@@ -1031,8 +1031,8 @@ std::unique_ptr<sst_plan> create_plan(const sst_plan_desc* d, int device, int fo
             if (gh.patch_w <= 256 && P->h16.launch) {
                 P->img_h = stensor::build_device_image(gh, d->rows, d->cols, d->a_values, d->a_meta, origin.data(),
                                                        d->window_w, d->window_h);
-                ck(cudaMalloc(&P->d_gsrc_h, P->img_h.gather_src.size() * 4), "cudaMalloc");
-                ck(cudaMemcpy(P->d_gsrc_h, P->img_h.gather_src.data(), P->img_h.gather_src.size() * 4,
+                ck(cudaMalloc(&P->d_gsrc_h, P->img_h.gather_packed.size() * 4), "cudaMalloc");
+                ck(cudaMemcpy(P->d_gsrc_h, P->img_h.gather_packed.data(), P->img_h.gather_packed.size() * 4,
                               cudaMemcpyHostToDevice), "cudaMemcpy");
                 ck(cudaMalloc(&P->d_gdst_h, P->img_h.gather_dst.size() * 4), "cudaMalloc");
                 ck(cudaMemcpy(P->d_gdst_h, P->img_h.gather_dst.data(), P->img_h.gather_dst.size() * 4,
@@ -1047,8 +1047,8 @@ std::unique_ptr<sst_plan> create_plan(const sst_plan_desc* d, int device, int fo
         ck(cudaMalloc(&P->d_e, P->img.e_words.size() * 4), "cudaMalloc");
         ck(cudaMemcpy(P->d_e, P->img.e_words.data(), P->img.e_words.size() * 4, cudaMemcpyHostToDevice),
            "cudaMemcpy");
-        ck(cudaMalloc(&P->d_gsrc, P->img.gather_src.size() * 4), "cudaMalloc");
-        ck(cudaMemcpy(P->d_gsrc, P->img.gather_src.data(), P->img.gather_src.size() * 4,
+        ck(cudaMalloc(&P->d_gsrc, P->img.gather_packed.size() * 4), "cudaMalloc");
+        ck(cudaMemcpy(P->d_gsrc, P->img.gather_packed.data(), P->img.gather_packed.size() * 4,
                       cudaMemcpyHostToDevice),
            "cudaMemcpy");
         ck(cudaMalloc(&P->d_gdst, P->img.gather_dst.size() * 4), "cudaMalloc");

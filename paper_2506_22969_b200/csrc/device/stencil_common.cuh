@@ -39,8 +39,9 @@ struct PeerMaps {
 struct StepParams {
     const uint4* a_img;        // A'' smem image (fp16), nks * 4096 bytes
     const uint32_t* e_words;   // [nks][128]
-    const int32_t* gsrc;       // [k_pad/32][32] patch byte offset of the lane's B'' row
-    const int32_t* gdst;       // [k_pad/32][32] byte offset of that row in an 8-tile group
+    const int32_t* gsrc;       // [k_pad/32][32] packed: (patch byte offset of the lane's B'' row) / 2
+                               //   | (that row's index in an 8-tile group) << 16
+    const int32_t* gdst;       // [k_pad/32][32] the row's byte offset (unpacked; staged, not read)
     float* buf[2];             // ping-pong storage buffers (right-edge columns, see epilogue)
     int32_t src;               // buffer holding the input of the launch's first step
     int32_t nsteps;            // time steps (operator applications) in this launch
@@ -201,10 +202,12 @@ __device__ __forceinline__ void gather_sweeps(uint32_t pbase, uint32_t bbase, co
                                               uint32_t lane, const int32_t (&toff)[GPW][8]) {
     uint32_t src[UNR], dst[UNR];
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-        src[u] = pbase + static_cast<uint32_t>(sGsrc[(j0 + u) * 32 + lane]);
-        dst[u] = bbase + static_cast<uint32_t>(sGdst[(j0 + u) * 32 + lane]);
+    for (int u = 0; u < UNR; ++u) {  // packed table: one load per lane and sweep
+        const uint32_t e = static_cast<uint32_t>(sGsrc[(j0 + u) * 32 + lane]);
+        src[u] = pbase + ((e & 0xffffu) << 1);
+        dst[u] = bbase + ((e >> 16) << 4);
     }
+    (void)sGdst;
     if constexpr (HIN) {
         static_assert(!LO, "split operands need fp32 storage");
         uint32_t hv[UNR][GPW][8];

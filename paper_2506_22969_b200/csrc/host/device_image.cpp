@@ -220,6 +220,15 @@ DeviceImage build_device_image(const BatchGeometry& geo_in, std::size_t rows, st
         }
         g.k_pad = static_cast<int>(2 * k_pad);
     }
+    // the kernels read ONE 32-bit word per lane and sweep: half the patch byte offset
+    // (low 16 bits; offsets are even, patches < 128 KiB) | the B'' row (high 16 bits)
+    img.gather_packed.resize(img.gather_src.size());
+    for (std::size_t i = 0; i < img.gather_src.size(); ++i) {
+        const std::int32_t src = img.gather_src[i], row = img.gather_dst[i] / 16;
+        if (src < 0 || src >= (1 << 17) || (src & 1) || row >= (1 << 16))
+            throw std::invalid_argument("gather table entry out of the packed range");
+        img.gather_packed[i] = (src >> 1) | (row << 16);
+    }
     return img;
 }
 

@@ -38,6 +38,8 @@ struct DeviceImage {
     // flattened schedule, [k_pad/32][32]: lane's patch byte offset and its
     // byte offset inside one 8-tile B'' group (MN-major: row k at k * 16 B)
     std::vector<std::int32_t> gather_src, gather_dst;
+    // what the kernels load: (gather_src / 2) | (gather_dst / 16) << 16 per lane and sweep
+    std::vector<std::int32_t> gather_packed;
     int worst_bank_conflict = 0;          // max lanes per bank over gather LDS sweeps
     int lo_sweep0 = 0;                    // first gather sweep producing B_lo rows (= sweeps if terms 1)
 };
