@@ -152,8 +152,8 @@ sst_status sst_multi_create(const sst_plan_desc* global, int nslabs, const int* 
                     ck(e, "cudaDeviceEnablePeerAccess");
             }
         }
-        // binary16 pairs too (3D f16 plans), so runs keep binary16 between steps
-        const bool h16 = global->dims == 3 && global->precision == SST_PREC_F16;
+        // binary16 pairs too (f16 plans), so runs keep binary16 between steps
+        const bool h16 = global->precision == SST_PREC_F16;
         auto wire = [&](Slab& s, int which, const Slab& nb) {
             void *b0 = nullptr, *b1 = nullptr;
             check(sst_plan_buffers(nb.plan, &b0, &b1));

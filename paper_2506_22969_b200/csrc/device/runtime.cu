@@ -197,9 +197,11 @@ __global__ void ring_to_half_kernel(const float* __restrict__ src, __half* __res
     // z planes converted whole: [0, zl) and [gz - zh, gz); the others [zl, gz - zh) like interior planes
     const int zl = d3 && !halo_lo ? r : 0, zh = d3 && !halo_hi ? r : 0;
     const int nin = d3 ? gz - zl - zh : 1;  // planes converted ring-only
+    // 2D slabs: the r halo rows at a peer end are converted like interior rows (x ring only)
+    const int yl = !d3 && halo_lo ? 0 : r, yh = !d3 && halo_hi ? 0 : r;  // whole ring rows per plane
     const long long full_planes_rows = static_cast<long long>(zl + zh) * gy;  // rows of the whole planes
-    const long long full_rows = full_planes_rows + 2LL * r * nin;            // + y ring rows
-    const long long inner_rows = static_cast<long long>(gy - 2 * r) * nin;
+    const long long full_rows = full_planes_rows + static_cast<long long>(yl + yh) * nin;  // + y ring rows
+    const long long inner_rows = static_cast<long long>(gy - yl - yh) * nin;
     const long long n_full = full_rows * gx, n_all = n_full + inner_rows * 2 * r;
     for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_all;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -213,17 +215,17 @@ __global__ void ring_to_half_kernel(const float* __restrict__ src, __half* __res
                 z = pz < zl ? pz : gz - zh - zl + pz;
             } else {
                 const long long g = f - full_planes_rows;
-                const int j = static_cast<int>(g % (2 * r));
-                z = d3 ? zl + static_cast<int>(g / (2 * r)) : 0;
-                y = j < r ? j : gy - 2 * r + j;
+                const int j = static_cast<int>(g % (yl + yh));
+                z = d3 ? zl + static_cast<int>(g / (yl + yh)) : 0;
+                y = j < yl ? j : gy - yl - yh + j;
             }
         } else {
             const long long g = i - n_full;
             const long long row = g / (2 * r);
             const int j = static_cast<int>(g % (2 * r));
             x = j < r ? j : gx - 2 * r + j;
-            y = r + static_cast<int>(row % (gy - 2 * r));
-            z = d3 ? zl + static_cast<int>(row / (gy - 2 * r)) : 0;
+            y = yl + static_cast<int>(row % (gy - yl - yh));
+            z = d3 ? zl + static_cast<int>(row / (gy - yl - yh)) : 0;
         }
         const __half h = __float2half_rn(src[z * pp + y * rp + lp + x]);
         const long long o = z * pph + y * rph + lph + x;
@@ -304,6 +306,8 @@ struct sst_plan {
     sst_storage storage_h{};
     int load_x0_h = 0;
     __half* hbuf[2] = {nullptr, nullptr};
+    __half* hbuf_base[2] = {nullptr, nullptr};  // allocations (2D: kGuardRows rows before hbuf, as buf)
+    int64_t guard_elems_h() const { return dims == 2 ? kGuardRows * static_cast<int64_t>(storage_h.row_pitch) : 0; }
     CUtensorMap hin[2]{}, hout[2]{};  // f16 patch loads / interior stores
     CUtensorMap hring[2]{};           // 3D: the f16 buffers' right-edge ring chunks (kEdgeRing)
     // 3D slabs with P2P halos in binary16 runs: the neighbours' binary16 buffers
@@ -335,8 +339,8 @@ struct sst_plan {
         cudaFree(d_peer_maps_run);
         cudaFree(d_gsrc_h);
         cudaFree(d_gdst_h);
-        cudaFree(hbuf[0]);
-        cudaFree(hbuf[1]);
+        cudaFree(hbuf_base[0]);
+        cudaFree(hbuf_base[1]);
         if (owns_buf) {
             cudaFree(alloc_base[0]);
             cudaFree(alloc_base[1]);
@@ -554,11 +558,12 @@ struct sst_plan {
     // binary16 storage buffers and their tensor maps (allocated on first use)
     void ensure_h16() {
         if (hmaps_ok) return;
-        const size_t bytes = storage_h.bytes;
+        const size_t bytes = storage_h.bytes + static_cast<size_t>(guard_elems_h()) * 2;
         for (int i = 0; i < 2; ++i) {
-            if (!hbuf[i]) {
-                ck(cudaMalloc(&hbuf[i], bytes), "cudaMalloc(f16 grid)");
-                ck(cudaMemset(hbuf[i], 0, bytes), "cudaMemset(f16 grid)");
+            if (!hbuf_base[i]) {
+                ck(cudaMalloc(&hbuf_base[i], bytes), "cudaMalloc(f16 grid)");
+                ck(cudaMemset(hbuf_base[i], 0, bytes), "cudaMemset(f16 grid)");
+                hbuf[i] = hbuf_base[i] + guard_elems_h();
             }
         }
         const cuuint64_t gstride[2] = {storage_h.row_pitch * 2, storage_h.plane_pitch * 2};
@@ -608,6 +613,29 @@ struct sst_plan {
     // the PeerMaps of binary16 slab runs (see d_peer_maps_run)
     void make_run_peer_maps() {
         sst::PeerMaps pm[4]{};
+        if (dims == 2) {  // rows: upper neighbour's last r rows; lower neighbour's first r (map from its guard)
+            const cuuint64_t gstride[1] = {storage_h.row_pitch * 2};
+            const int ox8 = (gx - 2 * r) & ~7;
+            const cuuint32_t obox[2] = {64u, static_cast<cuuint32_t>(tiles_y * sst::kTileH)};
+            const int64_t inner0 = static_cast<int64_t>(storage_h.left_pad) + r;
+            for (int w = 0; w < 2; ++w) {
+                if (!peer_buf[w][0]) continue;
+                const int64_t guard = w == 1 ? kGuardRows : 0;
+                const int64_t first = w == 0 ? static_cast<int64_t>(peer_slices[0]) - r : -guard;
+                for (int i = 0; i < 2; ++i) {
+                    __half* base = peer_hbuf[w][i] + first * static_cast<int64_t>(storage_h.row_pitch) + inner0;
+                    const cuuint64_t pdim[2] = {static_cast<cuuint64_t>(std::max(ox8, 8)),
+                                                static_cast<cuuint64_t>(r + guard)};
+                    encode(w == 0 ? &pm[i].up[1] : &pm[i].down[1], 2, base, pdim, gstride, obox,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+                    (w == 0 ? pm[2 + i].up[1] : pm[2 + i].down[1]) = w == 0 ? peer_maps_h.up[i] : peer_maps_h.down[i];
+                }
+            }
+            if (!d_peer_maps_run) ck(cudaMalloc(&d_peer_maps_run, sizeof pm), "cudaMalloc(run peer maps)");
+            ck(cudaMemcpy(d_peer_maps_run, pm, sizeof pm, cudaMemcpyHostToDevice), "cudaMemcpy(run peer maps)");
+            run_maps_ok = true;
+            return;
+        }
         const cuuint64_t gstride[2] = {storage_h.row_pitch * 2, storage_h.plane_pitch * 2};
         const int ox = gx - 2 * r, ox8 = ox & ~7, oxs = (ox & 7) ? ox8 + 8 : ox8;
         const cuuint32_t obox[3] = {64u, static_cast<cuuint32_t>(tiles_y * sst::kTileH), 1u};
@@ -659,8 +687,9 @@ struct sst_plan {
         const char* dyn_e = std::getenv("SST_DYN");
         // (the store-only ablation, debug bit 32, has no producer to draw batches)
         // (the 3D stream kernel splits its work statically)
+        // (2D slab peers: only the dynamic-peer instantiation carries the peer stores)
         const bool dyn = variant->kz == 0 && !(debug_mode & 32) &&
-                         (dyn_e ? std::atoi(dyn_e) != 0 : p.nbatch >= 8 * grid);
+                         (p.peer_mask != 0 || (dyn_e ? std::atoi(dyn_e) != 0 : p.nbatch >= 8 * grid));
         if (dyn && !d_sched) {
             ck(cudaMalloc(&d_sched, 4), "cudaMalloc(sched)");
             ck(cudaMemsetAsync(d_sched, 0, 4, st), "cudaMemsetAsync(sched)");
@@ -668,7 +697,13 @@ struct sst_plan {
         }
         p.sched = dyn ? d_sched : nullptr;
         p.sched_base = sched_base;
-        if (p.peer_mask) p.peer_maps = d_peer_maps_run + (ho ? static_cast<int>(t & 1) : 2 + fin);
+        if (p.peer_mask) {  // the launch's output parity is [1] (p.src = 0)
+            p.peer_maps = d_peer_maps_run + (ho ? static_cast<int>(t & 1) : 2 + fin);
+            for (int w = 0; w < 2; ++w) {  // 2D plain right-edge peer stores
+                float* nb = ho ? reinterpret_cast<float*>(peer_hbuf[w][t & 1]) : peer_buf[w][fin];
+                (w == 0 ? p.peer_up_buf : p.peer_down_buf)[1] = nb;
+            }
+        }
         h16.launch(dyn, hi, ho, grid, hi ? smem_h : smem_f32_h, st, m, p);
         if (dyn)
             sched_base += static_cast<uint32_t>((p.nbatch + sst::kDrawGroup - 1) / sst::kDrawGroup +
@@ -696,7 +731,7 @@ struct sst_plan {
         // slab peers: 3D only, and every fp32 peer must have its binary16 buffers too
         bool peers_ok = true;
         for (int w = 0; w < 2; ++w)
-            if (peer_buf[w][0]) peers_ok &= dims == 3 && hp->peer_buf[w][0] && hp->peer_hbuf[w][0];
+            if (peer_buf[w][0]) peers_ok &= hp->peer_buf[w][0] && hp->peer_hbuf[w][0] && y_lo2 == 0;
         if (hp->h16_ok && h16_enabled() && !multi && full && nsteps > 1 && peers_ok) return hp;
         return nullptr;
     }
@@ -1311,8 +1346,8 @@ sst_status sst_plan_buffers_h(sst_plan* plan, void** h0, void** h1) {
         if (!hp->h16_ok) throw std::invalid_argument("plan has no binary16 storage");
         ck(cudaSetDevice(hp->device), "cudaSetDevice");
         hp->ensure_h16();
-        *h0 = hp->hbuf[0];
-        *h1 = hp->hbuf[1];
+        *h0 = hp->hbuf_base[0];  // allocation starts (2D: guard rows first), like sst_plan_buffers
+        *h1 = hp->hbuf_base[1];
         return SST_OK;
     } catch (...) {
         return sstc::from_current_exception();
@@ -1326,8 +1361,9 @@ sst_status sst_plan_set_peer_h(sst_plan* plan, int which, void* h0, void* h1) {
         if ((h0 == nullptr) != (h1 == nullptr)) throw std::invalid_argument("peer needs both buffers");
         if (h0 && !plan->peer_buf[which][0]) throw std::invalid_argument("set the fp32 peer (sst_plan_set_peer) first");
         sst_plan* hp = plan->typed ? plan->typed.get() : plan;
-        hp->peer_hbuf[which][0] = static_cast<__half*>(h0);
-        hp->peer_hbuf[which][1] = static_cast<__half*>(h1);
+        // peers are sst_plan_buffers_h allocations: skip their guard rows
+        hp->peer_hbuf[which][0] = h0 ? static_cast<__half*>(h0) + hp->guard_elems_h() : nullptr;
+        hp->peer_hbuf[which][1] = h1 ? static_cast<__half*>(h1) + hp->guard_elems_h() : nullptr;
         hp->run_maps_ok = false;
         return SST_OK;
     } catch (...) {

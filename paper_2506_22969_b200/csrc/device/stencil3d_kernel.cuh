@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 if constexpr (HOUT) {
                     if (!(p.debug_mode & 1))
-                        store_batch_h<3, TYB, NS, kEdgeRing>(
+                        store_batch_h<3, TYB, NS, kEdgeRing, PEER>(
                             p, tmap_out, reinterpret_cast<__half*>(buf_of(p, p.src ^ 1)), v, sS, L.s_stride, o, X0,
                             Y0, p.slow_lo + zo, q, lane, etid, reinterpret_cast<const __half*>(ring),
                             (PEER && (p.peer_mask & 1)) ? &p.peer_maps->up[p.src ^ 1] : nullptr,

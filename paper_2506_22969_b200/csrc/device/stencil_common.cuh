@@ -550,15 +550,43 @@ __device__ __forceinline__ void store_right_edge_h(const StepParams& p, __half* 
 // map runs to ox8 + 8 and the cells [ox, ox8 + 8) of that last 16-byte chunk are
 // staged with the output storage's own (constant) binary16 values from `ring`
 // (TYB*8 rows x 8 halves).
-// peer_up / peer_down (3D slabs with P2P halos): the neighbours' binary16 halo
-// planes, stored from the same staged boxes as in store_batch.
-template <int DIMS, int TYB, int NS, int EDGE = kEdgePlain>
+// Slab P2P halos, 2D binary16: the <= 7 right-edge columns [ox8, ox) of the
+// neighbours' halo rows (TMA clips them), copied from the staged binary16 boxes.
+__device__ __forceinline__ void peer_right_edge_h(const StepParams& p, uint32_t stage, uint32_t s_stride, int X0,
+                                                  int Y0, int rows, __half* up, __half* down, uint32_t lane) {
+    const int ox = p.gx - 2 * p.r, ox8 = ox & ~7;
+    if (X0 + kTXB * kTileW <= ox8 || ox8 == ox) return;
+    const int w = ox - ox8;
+    for (int e = static_cast<int>(lane); e < rows * w; e += 32) {
+        const int yl = e / w, x = ox8 + e % w, y = Y0 + yl;
+        const bool to_up = up != nullptr && y < p.r, to_down = down != nullptr && y >= p.peer_down0;
+        if (!(to_up || to_down) || y >= p.slow_hi) continue;
+        const int xl = x - X0;  // box xl / 64, 16-byte chunk (xl % 64) / 8 swizzled with the row
+        unsigned short bits;
+        asm volatile("ld.shared.u16 %0, [%1];"
+                     : "=h"(bits)
+                     : "r"(stage + static_cast<uint32_t>(xl / 64) * s_stride + static_cast<uint32_t>(yl) * 128u +
+                           (static_cast<uint32_t>(((xl % 64) / 8) ^ (yl % 8)) * 16u) +
+                           static_cast<uint32_t>(xl % 8) * 2u));
+        const __half val = *reinterpret_cast<const __half*>(&bits);
+        const int64_t off = static_cast<int64_t>(y + p.r) * p.row_pitch + p.left_pad + p.r + x;
+        if (to_up) up[off + p.peer_up_shift * p.row_pitch] = val;
+        if (to_down) down[off + p.peer_down_shift * p.row_pitch] = val;
+    }
+}
+
+// PEER (slabs with P2P halos; only the instantiations launched with peers carry the
+// code): peer_up / peer_down are the neighbours' binary16 halo slices, stored from the
+// same staged boxes as in store_batch; 2D also copies the <= 7 right-edge columns
+// into peer_up_buf / peer_down_buf.
+template <int DIMS, int TYB, int NS, int EDGE = kEdgePlain, bool PEER = false>
 __device__ __forceinline__ void store_batch_h(const StepParams& p, const CUtensorMap* tmap_out, __half* dst,
                                               uint32_t (&v)[kTXB / 2][2 * TYB], uint8_t* sS,
                                               uint32_t s_stride, int nb, int X0, int Y0, int Z0, uint32_t q,
                                               uint32_t lane, int etid, const __half* ring = nullptr,
                                               const CUtensorMap* peer_up = nullptr,
-                                              const CUtensorMap* peer_down = nullptr) {
+                                              const CUtensorMap* peer_down = nullptr,
+                                              __half* peer_up_buf = nullptr, __half* peer_down_buf = nullptr) {
     using namespace ptx;
     constexpr int CW = 2 * TYB, NBOX = kTXB / 2;
     constexpr int HBOX = 64;  // halves per 128-byte box row
@@ -605,6 +633,9 @@ __device__ __forceinline__ void store_batch_h(const StepParams& p, const CUtenso
                          : "memory");
         }
     named_bar_sync(kEpiBarrier, kEpiWarps * 32);
+    if constexpr (DIMS == 2 && PEER)
+        if (p.peer_mask != 0 && etid >= 32 && etid < 64 && (Y0 < p.r || Y0 + TYB * kTileH > p.peer_down0))
+            peer_right_edge_h(p, stage, s_stride, X0, Y0, TYB * kTileH, peer_up_buf, peer_down_buf, lane);
     if (etid == 0 && !(p.debug_mode & 64)) {
         fence_proxy_async_smem();
 #pragma unroll
@@ -616,7 +647,25 @@ __device__ __forceinline__ void store_batch_h(const StepParams& p, const CUtenso
             else
                 tma_store_3d(tmap_out, sS + buf + cb * s_stride, bx0, Y0, Z0);
         }
-        if constexpr (DIMS == 3) {
+        if constexpr (PEER && DIMS == 2) {  // (the lower neighbour's map starts in its guard rows)
+            if (peer_up != nullptr && Y0 < p.r) {
+#pragma unroll 1
+                for (int cb = 0; cb < NBOX / 2; ++cb) {
+                    const int bx0 = X0 + cb * HBOX;
+                    if (bx0 >= oxs) break;
+                    tma_store_2d(peer_up, sS + buf + cb * s_stride, bx0, Y0);
+                }
+            }
+            if (peer_down != nullptr && Y0 + TYB * kTileH > p.peer_down0) {
+#pragma unroll 1
+                for (int cb = 0; cb < NBOX / 2; ++cb) {
+                    const int bx0 = X0 + cb * HBOX;
+                    if (bx0 >= oxs) break;
+                    tma_store_2d(peer_down, sS + buf + cb * s_stride, bx0, Y0 - p.peer_down_c0);
+                }
+            }
+        }
+        if constexpr (PEER && DIMS == 3) {
             if (peer_up != nullptr && Z0 < p.r) {
 #pragma unroll 1
                 for (int cb = 0; cb < NBOX / 2; ++cb) {

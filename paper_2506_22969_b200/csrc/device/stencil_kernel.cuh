@@ -537,10 +537,14 @@ __global__ void __launch_bounds__(kThreads, CPS)
             if constexpr (DIMS == 2 && !HOUT)
                 if (p.fold_ring != nullptr) fold_keep_ring<TYB>(p, v, X0, Y0, q, lane);
             if constexpr (HOUT) {
+                const int par = (p.src + t + 1) & 1;
                 if (!(p.debug_mode & 1))
-                    store_batch_h<DIMS, TYB, NS>(p, &maps.out[(p.src + t + 1) & 1],
-                                                 reinterpret_cast<__half*>(buf_of(p, (p.src + t + 1) & 1)), v, sS,
-                                                 L.s_stride, r - 1, X0, Y0, Z0, q, lane, etid);
+                    store_batch_h<DIMS, TYB, NS, kEdgePlain, MODE == kModePeer>(
+                        p, &maps.out[par], reinterpret_cast<__half*>(buf_of(p, par)), v, sS, L.s_stride, r - 1, X0,
+                        Y0, Z0, q, lane, etid, nullptr, (p.peer_mask & 1) ? &p.peer_maps->up[par] : nullptr,
+                        (p.peer_mask & 2) ? &p.peer_maps->down[par] : nullptr,
+                        reinterpret_cast<__half*>(par ? p.peer_up_buf[1] : p.peer_up_buf[0]),
+                        reinterpret_cast<__half*>(par ? p.peer_down_buf[1] : p.peer_down_buf[0]));
             } else if (!(p.debug_mode & 1))
             {
                 const int par = (p.src + t + 1) & 1;

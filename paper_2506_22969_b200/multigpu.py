@@ -212,10 +212,10 @@ class SlabStencil:
             check(L.sst_ipc_handle(C.c_void_p(ptr), h))
             return bytes(h)
 
-        # 3D f16 plans also export their binary16 pair: runs then keep binary16 between
+        # f16 plans also export their binary16 pair: runs then keep binary16 between
         # steps, halos included (sst_plan_set_peer_h)
         hbufs = None
-        if len(self.local_dims) == 3 and self.precision == "f16":
+        if self.precision == "f16":
             h0, h1 = C.c_void_p(), C.c_void_p()
             if L.sst_plan_buffers_h(self.eng._h, C.byref(h0), C.byref(h1)) == 0:
                 hbufs = [handle(h0.value), handle(h1.value)]

@@ -101,9 +101,10 @@ def test_explorer_choice_runs_on_the_device(gpu, name, dims):
 
 
 @pytest.mark.parametrize("name,dims,nslabs", [("Box-3D27P", (40, 36, 70), 3), ("Heat-3D", (33, 17, 129), 2),
-                                              ("Box-3D27P", (24, 40, 133), 4)])
-def test_multi_3d_binary16_halos(gpu, name, dims, nslabs):
-    """3D slabs keep binary16 between steps, halos included (the neighbours' binary16
+                                              ("Box-3D27P", (24, 40, 133), 4), ("Box-2D9P", (257, 300), 3),
+                                              ("Star-2D13P", (160, 133), 2), ("Heat-2D", (130, 517), 4)])
+def test_multi_binary16_halos(gpu, name, dims, nslabs):
+    """Slabs keep binary16 between steps, halos included (the neighbours' binary16
     pairs registered with sst_plan_set_peer_h): bitwise the single-domain sweep, every
     launch a binary16 one, across repeated runs."""
     g = oracle.random_grid(dims, seed=31).astype(np.float32)

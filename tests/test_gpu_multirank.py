@@ -85,8 +85,8 @@ def test_two_ranks_equal_single_domain(gpu, tmp_path, name, owned, rest, steps, 
         assert np.array_equal(rows, full[g0:g0 + len(rows)]), (rank, np.abs(rows - full[g0:g0 + len(rows)]).max())
         # nccl: interior window + one boundary window per step; p2p: one launch per step
         assert launches == (steps // fuse) * (2 if halo == "nccl" else 1)
-        # 3D p2p slabs keep binary16 between steps, halos included (IPC-mapped binary16 pairs)
-        assert h16 == (steps // fuse if (halo == "p2p" and len(rest) == 2) else 0)
+        # p2p slabs keep binary16 between steps, halos included (IPC-mapped binary16 pairs)
+        assert h16 == (steps // fuse if halo == "p2p" else 0)
 
 
 @pytest.mark.parametrize("name,owned,rest,steps", [("Box-2D9P", 100, (203,), 5), ("Box-3D27P", 16, (30, 70), 4),
