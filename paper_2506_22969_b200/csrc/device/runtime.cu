@@ -610,45 +610,28 @@ struct sst_plan {
         if ((peer_buf[0][0] || peer_buf[1][0]) && !run_maps_ok) make_run_peer_maps();
     }
 
-    // the PeerMaps of binary16 slab runs (see d_peer_maps_run)
+    // the PeerMaps of binary16 slab runs (see d_peer_maps_run): the neighbours' binary16
+    // halo slices as this rank's interior coordinates address them (2D: rows, the lower
+    // neighbour's map starting in its guard rows; 3D: planes), and the fp32 ones
     void make_run_peer_maps() {
         sst::PeerMaps pm[4]{};
-        if (dims == 2) {  // rows: upper neighbour's last r rows; lower neighbour's first r (map from its guard)
-            const cuuint64_t gstride[1] = {storage_h.row_pitch * 2};
-            const int ox8 = (gx - 2 * r) & ~7;
-            const cuuint32_t obox[2] = {64u, static_cast<cuuint32_t>(tiles_y * sst::kTileH)};
-            const int64_t inner0 = static_cast<int64_t>(storage_h.left_pad) + r;
-            for (int w = 0; w < 2; ++w) {
-                if (!peer_buf[w][0]) continue;
-                const int64_t guard = w == 1 ? kGuardRows : 0;
-                const int64_t first = w == 0 ? static_cast<int64_t>(peer_slices[0]) - r : -guard;
-                for (int i = 0; i < 2; ++i) {
-                    __half* base = peer_hbuf[w][i] + first * static_cast<int64_t>(storage_h.row_pitch) + inner0;
-                    const cuuint64_t pdim[2] = {static_cast<cuuint64_t>(std::max(ox8, 8)),
-                                                static_cast<cuuint64_t>(r + guard)};
-                    encode(w == 0 ? &pm[i].up[1] : &pm[i].down[1], 2, base, pdim, gstride, obox,
-                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
-                    (w == 0 ? pm[2 + i].up[1] : pm[2 + i].down[1]) = w == 0 ? peer_maps_h.up[i] : peer_maps_h.down[i];
-                }
-            }
-            if (!d_peer_maps_run) ck(cudaMalloc(&d_peer_maps_run, sizeof pm), "cudaMalloc(run peer maps)");
-            ck(cudaMemcpy(d_peer_maps_run, pm, sizeof pm, cudaMemcpyHostToDevice), "cudaMemcpy(run peer maps)");
-            run_maps_ok = true;
-            return;
-        }
+        const int ox = gx - 2 * r, ox8 = ox & ~7;
+        const int oxs = (dims == 3 && (ox & 7)) ? ox8 + 8 : ox8;  // (3D: kEdgeRing stores the last chunk)
         const cuuint64_t gstride[2] = {storage_h.row_pitch * 2, storage_h.plane_pitch * 2};
-        const int ox = gx - 2 * r, ox8 = ox & ~7, oxs = (ox & 7) ? ox8 + 8 : ox8;
         const cuuint32_t obox[3] = {64u, static_cast<cuuint32_t>(tiles_y * sst::kTileH), 1u};
-        const int64_t inner0 = static_cast<int64_t>(r) * static_cast<int64_t>(storage_h.row_pitch) +
+        const int64_t slice_pitch = static_cast<int64_t>(dims == 3 ? storage_h.plane_pitch : storage_h.row_pitch);
+        const int64_t inner0 = (dims == 3 ? static_cast<int64_t>(r) * static_cast<int64_t>(storage_h.row_pitch) : 0) +
                                static_cast<int64_t>(storage_h.left_pad) + r;
         for (int w = 0; w < 2; ++w) {
             if (!peer_buf[w][0]) continue;
-            const int64_t first = w == 0 ? static_cast<int64_t>(peer_slices[0]) - r : 0;
+            const int64_t guard = (w == 1 && dims == 2) ? kGuardRows : 0;
+            const int64_t first = w == 0 ? static_cast<int64_t>(peer_slices[0]) - r : -guard;
             for (int i = 0; i < 2; ++i) {
-                __half* base = peer_hbuf[w][i] + first * static_cast<int64_t>(storage_h.plane_pitch) + inner0;
+                __half* base = peer_hbuf[w][i] + first * slice_pitch + inner0;
                 const cuuint64_t pdim[3] = {static_cast<cuuint64_t>(std::max(oxs, 8)),
-                                            static_cast<cuuint64_t>(gy - 2 * r), static_cast<cuuint64_t>(r)};
-                encode(w == 0 ? &pm[i].up[1] : &pm[i].down[1], 3, base, pdim, gstride, obox,
+                                            static_cast<cuuint64_t>(dims == 2 ? r + guard : gy - 2 * r),
+                                            static_cast<cuuint64_t>(r)};
+                encode(w == 0 ? &pm[i].up[1] : &pm[i].down[1], dims, base, pdim, gstride, obox,
                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
                 (w == 0 ? pm[2 + i].up[1] : pm[2 + i].down[1]) = w == 0 ? peer_maps_h.up[i] : peer_maps_h.down[i];
             }
@@ -728,10 +711,10 @@ struct sst_plan {
         const bool multi = ms_env && variant->multistep && full && nsteps > 1 && !fold_n && !peer_buf[0][0] &&
                            !peer_buf[1][0];
         sst_plan* hp = typed ? typed.get() : this;
-        // slab peers: 3D only, and every fp32 peer must have its binary16 buffers too
+        // slab peers: every fp32 peer must have its binary16 pair registered too
         bool peers_ok = true;
         for (int w = 0; w < 2; ++w)
-            if (peer_buf[w][0]) peers_ok &= hp->peer_buf[w][0] && hp->peer_hbuf[w][0] && y_lo2 == 0;
+            if (peer_buf[w][0]) peers_ok &= hp->peer_buf[w][0] && hp->peer_hbuf[w][0];
         if (hp->h16_ok && h16_enabled() && !multi && full && nsteps > 1 && peers_ok) return hp;
         return nullptr;
     }
