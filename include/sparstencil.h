@@ -226,7 +226,8 @@ SST_API sst_status sst_stream_wait_geq_u32(void* stream, uint32_t* dev_addr, uin
  * sst_run_steps; binary16 inter-step storage is used when every plan's run
  * qualifies (full window, no peers, f16, >= 2 operator steps), else fp32 single
  * steps. An ensemble of grids that each fit in L2 runs at the HBM-resident rate
- * (bench.py's small-grid timing). dst_out[i]: buffer holding plan i's result. */
+ * (bench.py's small-grid timing). dst_out[i]: buffer holding plan i's result.
+ * Plans with slab peers are refused (their neighbours' flags order their launches). */
 SST_API sst_status sst_run_steps_batch(sst_plan* const* plans, int n, const int* src, uint64_t steps, void* stream,
                                        int* dst_out);
 /* The per-step P2P schedule of one slab in C (what a rank of a multi-process run

@@ -1527,6 +1527,8 @@ sst_status sst_run_steps_batch(sst_plan* const* plans, int n, const int* src, ui
             if (!plans[i]->tmap_ok) throw std::invalid_argument("plan has no bound buffers");
             if (plans[i]->device != plans[0]->device) throw std::invalid_argument("plans on different devices");
             if (plans[i]->fuse != plans[0]->fuse) throw std::invalid_argument("plans with different fusion factors");
+            if (plans[i]->peer_buf[0][0] || plans[i]->peer_buf[1][0])
+                throw std::invalid_argument("slab plans with peers step through sst_run_steps_peer / sst_multi_run");
             for (int j = 0; j < i; ++j)
                 if (plans[j] == plans[i]) throw std::invalid_argument("a plan appears twice in the batch");
         }

@@ -419,6 +419,30 @@ static void image_tests() {
         const auto img = build_device_image(geo, 128, cv.converted.a.cols, a2.values.data(),
                                             a2.meta.data(), cv.converted.col_origin.data(), wv, wu);
         const int k_pad = img.geo.k_pad;
+        // the packed gather table the kernels read (one word per lane and sweep) covers
+        // every K row exactly once with its patch offset, for fp32 and binary16 patches
+        auto packed_ok = [&](const DeviceImage& im) {
+            std::vector<int> seen(static_cast<std::size_t>(im.geo.k_pad), 0);
+            bool good = im.gather_packed.size() == static_cast<std::size_t>(im.geo.k_pad);
+            for (std::size_t i = 0; good && i < im.gather_packed.size(); ++i) {
+                const uint32_t e = static_cast<uint32_t>(im.gather_packed[i]);
+                const uint32_t src = (e & 0xffffu) << 1, row = e >> 16;
+                good = row < seen.size() && src == static_cast<uint32_t>(im.koff[row] * im.geo.elem_bytes);
+                if (good) ++seen[row];
+            }
+            for (int c : seen) good = good && c == 1;
+            return good;
+        };
+        CHECK(packed_ok(img));
+        {
+            BatchGeometry gh = geo;
+            gh.elem_bytes = 2;
+            gh.x_shift = (8 - r % 8) % 8 & 7;
+            gh.patch_w = static_cast<int>((gh.x_shift + wv + 16 * 7 + 7) / 8 * 8);
+            const auto img_h = build_device_image(gh, 128, cv.converted.a.cols, a2.values.data(), a2.meta.data(),
+                                                  cv.converted.col_origin.data(), wv, wu);
+            CHECK(packed_ok(img_h));
+        }
         // decode A'' (dense, k_pad wide) back from the smem image + metadata words
         std::vector<double> A(128 * static_cast<std::size_t>(k_pad), 0.0);
         for (int m = 0; m < 128; ++m)
