@@ -67,9 +67,10 @@ def test_h16_wide_range_values(gpu):
     assert np.array_equal(ref.view(np.uint32), got.view(np.uint32))
 
 
-def test_h16_fused_operator(gpu):
+@pytest.mark.parametrize("fuse", [2, 4])
+def test_h16_fused_operator(gpu, fuse):
     g = oracle.random_grid((257, 300), seed=12).astype(np.float32)
-    ref, got, _ = run_both("Box-2D9P", g, 8, fuse=2)
+    ref, got, _ = run_both("Box-2D9P", g, 4 * fuse, fuse=fuse)
     assert np.array_equal(ref.view(np.uint32), got.view(np.uint32))
 
 
