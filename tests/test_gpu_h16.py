@@ -221,3 +221,14 @@ def test_run_batch_rejects_bad_batches(gpu):
             f.close()
     finally:
         e.close()
+
+
+@pytest.mark.parametrize("name,dims,steps", [("Box-2D9P", (8192, 8192), 1000), ("Box-3D27P", (512, 512, 512), 100),
+                                             ("Star-2D13P", (16384, 16384), 100)])
+def test_h16_baseline_configs_whole_grid_at_stated_T(gpu, name, dims, steps):
+    """The BASELINE configs at their stated T, whole grid: binary16 inter-step storage
+    is bitwise the fp32-storage sweep (so the per-config parity of the fp32 path,
+    test_gpu_baseline_parity.py, carries over cell for cell)."""
+    g = oracle.random_grid(dims, seed=1).astype(np.float32)
+    ref, got, _ = run_both(name, g, steps)
+    assert np.array_equal(ref.view(np.uint32), got.view(np.uint32))
