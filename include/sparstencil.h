@@ -332,6 +332,9 @@ SST_API sst_status sst_estimate_device(const char* stencil, const uint64_t* grid
 SST_API sst_status sst_random_grid(int ndims, const uint64_t* dims, uint64_t seed, float* out);
 SST_API const char* sst_last_error(void);
 SST_API int sst_device_count(void);
+/* Kernel launches the library has issued in this process (every kind: stencil steps,
+ * ring conversions, verification); a grouped batch step counts once. */
+SST_API unsigned long long sst_launch_count(void);
 SST_API const char* sst_version(void);
 
 #ifdef __cplusplus

@@ -29,7 +29,7 @@ EXPORTED = [
     "sst_ipc_open", "sst_ipc_close", "sst_stream_write_u32", "sst_stream_wait_geq_u32",
     "sst_run_steps_peer", "sst_download_slices", "sst_multi_create", "sst_multi_destroy", "sst_multi_upload",
     "sst_multi_run", "sst_multi_sync", "sst_multi_download", "sst_multi_slab", "sst_run_steps_multi",
-    "sst_estimate_device", "sst_run_steps_batch", "sst_plan_buffers_h", "sst_plan_set_peer_h",
+    "sst_estimate_device", "sst_run_steps_batch", "sst_plan_buffers_h", "sst_plan_set_peer_h", "sst_launch_count",
 ]
 
 
@@ -149,6 +149,7 @@ def lib() -> C.CDLL:
         "sst_random_grid": (i32, [i32, C.POINTER(u64), u64, P]),
         "sst_last_error": (C.c_char_p, []),
         "sst_device_count": (i32, []),
+        "sst_launch_count": (C.c_ulonglong, []),
         "sst_version": (C.c_char_p, []),
         "sst_run_compile": (i32, [C.POINTER(CompileRequest), C.POINTER(P)]),
         "sst_compile_result_destroy": (None, [P]),

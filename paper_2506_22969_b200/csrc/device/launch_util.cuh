@@ -6,6 +6,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -38,6 +39,12 @@ inline bool pdl_enabled() {
 }
 
 using KernelFn = void (*)(sst::MapSet, sst::StepParams);
+
+// kernel launches the library has issued, process-wide (sst_launch_count)
+inline std::atomic<unsigned long long>& launch_counter() {
+    static std::atomic<unsigned long long> n{0};
+    return n;
+}
 
 // cudaFuncAttributeMaxDynamicSharedMemorySize belongs to a kernel instantiation on a
 // device, not to a plan, and a plan's smem depends on its stencil. So the attribute
@@ -84,6 +91,7 @@ inline void launch_pdl(KernelFn fn, int grid, int smem, cudaStream_t st, const s
     cfg.attrs = attr;
     cfg.numAttrs = static_cast<unsigned>(na);
     ck(cudaLaunchKernelEx(&cfg, fn, maps, p), "cudaLaunchKernelEx");
+    launch_counter().fetch_add(1, std::memory_order_relaxed);
 }
 
 // Binary16-storage instantiations of one 2D variant (step_h16.cu): single-step

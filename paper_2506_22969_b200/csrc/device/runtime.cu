@@ -241,6 +241,7 @@ void sstl::launch_ring_to_half(const float* src, __half* d0, __half* d1, int gx,
     if (r == 0) return;
     ring_to_half_kernel<<<148 * 8, 256, 0, st>>>(src, d0, d1, gx, gy, gz, r, rp, pp, lp, rph, pph, lph,
                                                  halo_lo ? 1 : 0, halo_hi ? 1 : 0);
+    launch_counter().fetch_add(1, std::memory_order_relaxed);
 }
 
 struct sst_plan {
@@ -316,6 +317,8 @@ struct sst_plan {
     __half* peer_hbuf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
     sst::PeerMaps* d_peer_maps_run = nullptr;
     bool run_maps_ok = false;
+    sst::GroupMaps* d_group = nullptr;  // grouped batch runs (h16_run_group)
+    std::size_t group_cap = 0;
     bool hmaps_ok = false;
     uint64_t h16_launches = 0;        // launches that read or wrote binary16 storage
     int variant_index = -1;
@@ -337,6 +340,7 @@ struct sst_plan {
         cudaFree(d_ring_save);
         cudaFree(d_peer_maps);
         cudaFree(d_peer_maps_run);
+        cudaFree(d_group);
         cudaFree(d_gsrc_h);
         cudaFree(d_gdst_h);
         cudaFree(hbuf_base[0]);
@@ -641,12 +645,12 @@ struct sst_plan {
         run_maps_ok = true;
     }
 
-    void h16_step(int src, uint64_t t, uint64_t nsteps, cudaStream_t st) {
+    // launch t of a binary16 run of nsteps launches: parameters and tensor maps
+    sst::StepParams h16_params(int src, uint64_t t, uint64_t nsteps, sst::MapSet& m) const {
         const int fin = static_cast<int>((static_cast<uint64_t>(src) + nsteps) & 1);
         const bool hi = t > 0, ho = t + 1 < nsteps;
         sst::StepParams p = step_params(src);
-        const int grid = grid_size(p);
-        sst::MapSet m{};
+        m = sst::MapSet{};
         m.in[0] = m.in[1] = hi ? hin[(t - 1) & 1] : maps.in[src];
         m.out[0] = m.out[1] = ho ? hout[t & 1] : maps.out[fin];
         // 3D: the output storage's ring chunks (binary16: the output buffer's own,
@@ -667,19 +671,6 @@ struct sst_plan {
             p.gsrc = d_gsrc_h;
             p.gdst = d_gdst_h;
         }
-        const char* dyn_e = std::getenv("SST_DYN");
-        // (the store-only ablation, debug bit 32, has no producer to draw batches)
-        // (the 3D stream kernel splits its work statically)
-        // (2D slab peers: only the dynamic-peer instantiation carries the peer stores)
-        const bool dyn = variant->kz == 0 && !(debug_mode & 32) &&
-                         (p.peer_mask != 0 || (dyn_e ? std::atoi(dyn_e) != 0 : p.nbatch >= 8 * grid));
-        if (dyn && !d_sched) {
-            ck(cudaMalloc(&d_sched, 4), "cudaMalloc(sched)");
-            ck(cudaMemsetAsync(d_sched, 0, 4, st), "cudaMemsetAsync(sched)");
-            sched_base = 0;
-        }
-        p.sched = dyn ? d_sched : nullptr;
-        p.sched_base = sched_base;
         if (p.peer_mask) {  // the launch's output parity is [1] (p.src = 0)
             p.peer_maps = d_peer_maps_run + (ho ? static_cast<int>(t & 1) : 2 + fin);
             for (int w = 0; w < 2; ++w) {  // 2D plain right-edge peer stores
@@ -687,13 +678,96 @@ struct sst_plan {
                 (w == 0 ? p.peer_up_buf : p.peer_down_buf)[1] = nb;
             }
         }
+        return p;
+    }
+
+    // issue one launch of a binary16 run (items: batches to draw; group launches
+    // draw the batches of every grid of the group)
+    void h16_issue(sst::StepParams& p, const sst::MapSet& m, bool hi, bool ho, int items, cudaStream_t st) {
+        const int grid = grid_size(p);
+        const char* dyn_e = std::getenv("SST_DYN");
+        // (the store-only ablation, debug bit 32, has no producer to draw batches)
+        // (the 3D stream kernel splits its work statically)
+        // (2D slab peers and groups: only the dynamic instantiations carry them)
+        const bool dyn = variant->kz == 0 && !(debug_mode & 32) &&
+                         (p.peer_mask != 0 || p.group != nullptr ||
+                          (dyn_e ? std::atoi(dyn_e) != 0 : p.nbatch >= 8 * grid));
+        if (dyn && !d_sched) {
+            ck(cudaMalloc(&d_sched, 4), "cudaMalloc(sched)");
+            ck(cudaMemsetAsync(d_sched, 0, 4, st), "cudaMemsetAsync(sched)");
+            sched_base = 0;
+        }
+        p.sched = dyn ? d_sched : nullptr;
+        p.sched_base = sched_base;
         h16.launch(dyn, hi, ho, grid, hi ? smem_h : smem_f32_h, st, m, p);
         if (dyn)
-            sched_base += static_cast<uint32_t>((p.nbatch + sst::kDrawGroup - 1) / sst::kDrawGroup +
+            sched_base += static_cast<uint32_t>((items + sst::kDrawGroup - 1) / sst::kDrawGroup +
                                                 grid * (sst::kDrawAhead - 1));
         ck(cudaGetLastError(), "kernel launch");
         ++launches;
         ++h16_launches;
+    }
+
+    void h16_step(int src, uint64_t t, uint64_t nsteps, cudaStream_t st) {
+        sst::MapSet m;
+        sst::StepParams p = h16_params(src, t, nsteps, m);
+        h16_issue(p, m, t > 0, t + 1 < nsteps, p.nbatch, st);
+    }
+
+    // A grouped binary16 run: `this` (the runner of the group's first plan) launches
+    // every step once for all grids of `grp` (identical geometry and operators, see
+    // sst_run_steps_batch); d_group holds 4 x G GroupMaps: first launch, middle launches
+    // of even / odd t, last launch.
+    void h16_run_group(const std::vector<sst_plan*>& grp, const int* src, uint64_t L, cudaStream_t st) {
+        const std::size_t G = grp.size();
+        for (sst_plan* q : grp) q->ensure_h16();
+        std::vector<sst::GroupMaps> gm(4 * G);
+        for (std::size_t i = 0; i < G; ++i) {
+            const sst_plan* q = grp[i];
+            const int s0 = src[i], fin = static_cast<int>((static_cast<uint64_t>(s0) + L) & 1);
+            gm[i].in = q->maps.in[s0];  // first: fp32 in, binary16 out
+            gm[i].out = q->hout[0];
+            gm[i].out_buf = reinterpret_cast<float*>(q->hbuf[0]);
+            for (int par = 0; par < 2; ++par) {  // middle launch t (t & 1 = par): binary16 both ways
+                sst::GroupMaps& e = gm[(1 + par) * G + i];
+                e.in = q->hin[(par + 1) & 1];
+                e.out = q->hout[par];
+                e.out_buf = reinterpret_cast<float*>(q->hbuf[par]);
+            }
+            sst::GroupMaps& e = gm[3 * G + i];  // last: binary16 in, fp32 out
+            e.in = q->hin[(L - 2) & 1];
+            e.out = q->maps.out[fin];
+            e.out_buf = q->buf[fin];
+        }
+        if (group_cap < 4 * G) {
+            cudaFree(d_group);
+            d_group = nullptr;
+            ck(cudaMalloc(&d_group, 4 * G * sizeof(sst::GroupMaps)), "cudaMalloc(group maps)");
+            group_cap = 4 * G;
+        }
+        // pageable source: staged by the driver at the call, copied in stream order
+        ck(cudaMemcpyAsync(d_group, gm.data(), 4 * G * sizeof(sst::GroupMaps), cudaMemcpyHostToDevice, st),
+           "cudaMemcpyAsync(group maps)");
+        for (std::size_t i = 0; i < G; ++i) grp[i]->h16_begin(src[i], st);
+        for (uint64_t t = 0; t < L; ++t) {
+            sst::MapSet m;
+            sst::StepParams p = h16_params(src[0], t, L, m);
+            const int kind = t == 0 ? 0 : t + 1 == L ? 3 : 1 + static_cast<int>(t & 1);
+            p.group = d_group + static_cast<std::size_t>(kind) * G;
+            p.group_n = static_cast<int32_t>(G);
+            h16_issue(p, m, t > 0, t + 1 < L, p.nbatch * static_cast<int>(G), st);
+        }
+    }
+
+    // grids another runner can launch together with this one (same shape, stencil
+    // operator and storage: the constant operands and the tensor-map geometry agree)
+    bool groupable_with(const sst_plan* o) const {
+        return o->variant == variant && o->h16.launch == h16.launch && o->gx == gx && o->gy == gy && o->gz == gz &&
+               o->dims == dims && o->r == r && o->fuse == fuse && o->device == device && !fold_n && !o->fold_n &&
+               o->storage.row_pitch == storage.row_pitch && o->storage_h.row_pitch == storage_h.row_pitch &&
+               o->img.a_smem == img.a_smem && o->img.e_words == img.e_words &&
+               o->img.gather_packed == img.gather_packed && o->img_h.gather_packed == img_h.gather_packed &&
+               o->smem_h == smem_h && o->smem_f32_h == smem_f32_h && o->tmem_cols_h == tmem_cols_h;
     }
 
     int launch_h16(int src, uint64_t nsteps, cudaStream_t st) {
@@ -839,6 +913,8 @@ struct sst_plan {
 };
 
 extern "C" {
+
+unsigned long long sst_launch_count(void) { return sstl::launch_counter().load(); }
 
 int sst_device_count(void) {
     int n = 0;
@@ -1540,6 +1616,26 @@ sst_status sst_run_steps_batch(sst_plan* const* plans, int n, const int* src, ui
         bool all_h16 = true;
         for (int i = 0; i < n; ++i) all_h16 &= (hp[static_cast<std::size_t>(i)] = plans[i]->h16_runner(L)) != nullptr;
         std::vector<int> cur(src, src + n);
+        // identical 2D grids: ONE launch per step for the whole group (SST_GROUP=0: interleaved)
+        const char* grp_e = std::getenv("SST_GROUP");
+        bool group = all_h16 && n > 1 && L > 1 && !(grp_e && std::atoi(grp_e) == 0) && hp[0]->dims == 2;
+        for (int i = 1; i < n && group; ++i) group = hp[0]->groupable_with(hp[static_cast<std::size_t>(i)]);
+        if (group) {
+            sst_plan* h0p = hp[0];
+            const uint64_t l0 = h0p->launches, hh0 = h0p->h16_launches;
+            h0p->h16_run_group(hp, src, L, st);
+            const uint64_t dl = h0p->launches - l0, dh = h0p->h16_launches - hh0;
+            h0p->launches = l0;
+            h0p->h16_launches = hh0;
+            for (int i = 0; i < n; ++i) {  // every grid advanced L steps: count them on its plan
+                plans[i]->launches += dl;
+                plans[i]->h16_launches += dh;
+                cur[static_cast<std::size_t>(i)] = static_cast<int>((static_cast<uint64_t>(src[i]) + L) & 1);
+            }
+            if (dst_out)
+                for (int i = 0; i < n; ++i) dst_out[i] = cur[static_cast<std::size_t>(i)];
+            return SST_OK;
+        }
         if (all_h16) {
             std::vector<uint64_t> l0(static_cast<std::size_t>(n)), h0(static_cast<std::size_t>(n));
             for (int i = 0; i < n; ++i) {

@@ -36,6 +36,16 @@ struct PeerMaps {
     CUtensorMap down[2];
 };
 
+// Grouped launches (sst_run_steps_batch over identical grids): one launch advances every
+// grid of the group by one step; per grid its patch-load and store maps and its output
+// buffer, in global memory (TMA reads tensor maps from .global)
+struct GroupMaps {
+    CUtensorMap in;
+    CUtensorMap out;
+    float* out_buf;
+    uint64_t pad[15];  // 64-byte aligned entries
+};
+
 struct StepParams {
     const uint4* a_img;        // A'' smem image (fp16), nks * 4096 bytes
     const uint32_t* e_words;   // [nks][128]
@@ -83,6 +93,8 @@ struct StepParams {
     const float* fold_ring;    // 1D fold: the r right-ring cells' input values (else null)
     int64_t fold_nint;         // 1D fold: interior cells n_int = N - 2r (ring at [n_int, n_int + r))
     int32_t fold_w;            // 1D fold: interior cells per view row
+    const GroupMaps* group;    // grouped launch (kModeGroup): per grid maps, group_n grids of nbatch batches
+    int32_t group_n;
 };
 
 __device__ __forceinline__ float* buf_of(const StepParams& p, int i) {

@@ -143,7 +143,9 @@ __device__ __forceinline__ uint32_t refresh_min(const StepParams& p, uint32_t ne
 //     kPubEvery items, and whenever it idled 2 us, so no circular wait). Items of
 //     step t depend only on items drawn earlier, and a CTA holds only items it drew,
 //     so the schedule needs no co-residency.
-enum StepMode { kModeStatic = 0, kModeDynamic = 1, kModeMulti = 2, kModePeer = 3, kModeMultiDyn = 4 };
+//   5 grouped: dynamic batches over p.group_n identical grids (sst_run_steps_batch), item
+//     g = grid * nbatch + batch, the grid's maps and output buffer from p.group
+enum StepMode { kModeStatic = 0, kModeDynamic = 1, kModeMulti = 2, kModePeer = 3, kModeMultiDyn = 4, kModeGroup = 5 };
 
 // NS: output staging buffers (TMA stores of batch n read one while batch n + 1 stages
 // into the next; 1 = the epilogue waits for each batch's stores to leave smem)
@@ -264,8 +266,9 @@ __global__ void __launch_bounds__(kThreads, CPS)
     constexpr bool multi = MODE == kModeMulti;
     constexpr bool mdyn = MODE == kModeMultiDyn;
     // launches with a scheduler counter draw batches (mdyn: items) dynamically
-    constexpr bool dyn = MODE == kModeDynamic || MODE == kModePeer || mdyn;
-    const int nitems = mdyn ? p.nbatch * p.nsteps : p.nbatch;
+    constexpr bool grp = MODE == kModeGroup;
+    constexpr bool dyn = MODE == kModeDynamic || MODE == kModePeer || mdyn || grp;
+    const int nitems = mdyn ? p.nbatch * p.nsteps : grp ? p.nbatch * p.group_n : p.nbatch;
     int32_t* sPub = sBid + kBidSlots;  // mdyn: committed, unpublished items (epilogue etid 0)
     constexpr bool peer = MODE == kModePeer || DIMS == 3;  // (3D whole-window: one instantiation)
     auto next_bid = [&](int r) {  // consumers: batch index of real iteration r (-1: done)
@@ -311,7 +314,8 @@ __global__ void __launch_bounds__(kThreads, CPS)
                 }
                 g = __shfl_sync(0xffffffffu, g, 0);
                 if (g < 0) return false;
-                const int t = mdyn ? g / p.nbatch : 0, b = mdyn ? g - t * p.nbatch : g;
+                const int t = mdyn ? g / p.nbatch : 0, gj = grp ? g / p.nbatch : 0;
+                const int b = mdyn ? g - t * p.nbatch : grp ? g - gj * p.nbatch : g;
                 int X0, Y0, Z0;
                 batch_coords(b, X0, Y0, Z0);
                 if constexpr (mdyn) {
@@ -335,11 +339,17 @@ __global__ void __launch_bounds__(kThreads, CPS)
                     mbar_wait(&patch_empty[s], ((r / NP) & 1) ^ 1);
                     mbar_arrive_expect_tx(&patch_full[s], pbytes);
                     void* dst = sP + s * L.p_stride;
-                    const CUtensorMap* tin = &maps.in[(p.src + t) & 1];
-                    if (DIMS == 2)
-                        tma_load_2d(dst, tin, &patch_full[s], X0 + p.load_x0, Y0 + p.load_y0);
-                    else
-                        tma_load_3d(dst, tin, &patch_full[s], X0 + p.load_x0, Y0, Z0);
+                    // (kernel-parameter maps and global maps in separate instantiations: a pointer
+                    // that may be either is generic, and TMA faults on a generic param address)
+                    if constexpr (MODE == kModeGroup) {
+                        tma_load_2d(dst, &p.group[gj].in, &patch_full[s], X0 + p.load_x0, Y0 + p.load_y0);
+                    } else {
+                        const CUtensorMap* tin = &maps.in[(p.src + t) & 1];
+                        if (DIMS == 2)
+                            tma_load_2d(dst, tin, &patch_full[s], X0 + p.load_x0, Y0 + p.load_y0);
+                        else
+                            tma_load_3d(dst, tin, &patch_full[s], X0 + p.load_x0, Y0, Z0);
+                    }
                 }
                 __syncwarp();
                 ++r;
@@ -487,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
             published = upto;
         };
         for (int j = 0; dyn || j < total; ++j) {
-            int t = 0, b, X0, Y0, Z0;
+            int t = 0, b, X0, Y0, Z0, gj = 0;
             if constexpr (dyn) {
                 b = next_bid(r);
                 if (b < 0) break;
@@ -495,6 +505,10 @@ __global__ void __launch_bounds__(kThreads, CPS)
                     if (etid == 0) sPub[j % kPubRing] = b;
                     t = b / p.nbatch;
                     b -= t * p.nbatch;
+                }
+                if constexpr (grp) {
+                    gj = b / p.nbatch;
+                    b -= gj * p.nbatch;
                 }
             } else {
                 batch_of(j, t, b);
@@ -536,7 +550,16 @@ __global__ void __launch_bounds__(kThreads, CPS)
             }
             if constexpr (DIMS == 2 && !HOUT)
                 if (p.fold_ring != nullptr) fold_keep_ring<TYB>(p, v, X0, Y0, q, lane);
-            if constexpr (HOUT) {
+            if constexpr (grp) {  // grouped launch: the grid's map and buffer (global memory)
+                if constexpr (HOUT) {
+                    if (!(p.debug_mode & 1))
+                        store_batch_h<DIMS, TYB, NS>(p, &p.group[gj].out, reinterpret_cast<__half*>(p.group[gj].out_buf),
+                                                     v, sS, L.s_stride, r - 1, X0, Y0, Z0, q, lane, etid);
+                } else if (!(p.debug_mode & 1)) {
+                    store_batch<DIMS, TYB, NS, kEdgePlain, false>(p, &p.group[gj].out, p.group[gj].out_buf, v, sS,
+                                                                   L.s_stride, r - 1, X0, Y0, Z0, q, lane, etid);
+                }
+            } else if constexpr (HOUT) {
                 const int par = (p.src + t + 1) & 1;
                 if (!(p.debug_mode & 1))
                     store_batch_h<DIMS, TYB, NS, kEdgePlain, MODE == kModePeer>(

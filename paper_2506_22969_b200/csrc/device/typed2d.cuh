@@ -42,12 +42,19 @@ struct Typed2D {
         raise_smem_attr(k<sst::kModePeer, false, true>(), smem32);
         raise_smem_attr(k<sst::kModePeer, true, true>(), smem16);
         raise_smem_attr(k<sst::kModePeer, true, false>(), smem16);
+        raise_smem_attr(k<sst::kModeGroup, false, true>(), smem32);
+        raise_smem_attr(k<sst::kModeGroup, true, true>(), smem16);
+        raise_smem_attr(k<sst::kModeGroup, true, false>(), smem16);
     }
     static void launch(bool dyn, bool hin, bool hout, int grid, int smem, cudaStream_t st, const sst::MapSet& maps,
                        const sst::StepParams& p) {
         if (!hin && !hout) throw std::logic_error("typed launch without binary16 storage");
         KernelFn f = nullptr;
-        if (p.peer_mask) {  // slab P2P halos: the dynamic-peer instantiations (p.sched set)
+        if (p.group) {  // grouped launch over identical grids (sst_run_steps_batch)
+            if (!p.sched) throw std::logic_error("grouped launches draw batches dynamically");
+            f = hin ? (hout ? k<sst::kModeGroup, true, true>() : k<sst::kModeGroup, true, false>())
+                    : k<sst::kModeGroup, false, true>();
+        } else if (p.peer_mask) {  // slab P2P halos: the dynamic-peer instantiations (p.sched set)
             if (!p.sched) throw std::logic_error("peer launches draw batches dynamically");
             f = hin ? (hout ? k<sst::kModePeer, true, true>() : k<sst::kModePeer, true, false>())
                     : k<sst::kModePeer, false, true>();

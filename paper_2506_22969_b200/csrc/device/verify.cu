@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "../host/capi_internal.hpp"
+#include "launch_util.cuh"
 #include "stensor/pipeline.hpp"
 
 namespace {
@@ -190,9 +191,11 @@ double device_verify(const KernelPlan& plan, const StencilSpec& spec, const Grid
 
     ck(cudaEventRecord(e0), "cudaEventRecord");
     direct_step_kernel<<<static_cast<unsigned>((n_out + 255) / 256), 256>>>(da);
+    sstl::launch_counter().fetch_add(1);
     ck(cudaGetLastError(), "direct_step_kernel");
     if (nd > 0) {
         lut_sparse_kernel<<<static_cast<unsigned>((nd + 255) / 256), 256>>>(sa);
+        sstl::launch_counter().fetch_add(1);
         ck(cudaGetLastError(), "lut_sparse_kernel");
     }
     ck(cudaEventRecord(e1), "cudaEventRecord");

@@ -232,3 +232,40 @@ def test_h16_baseline_configs_whole_grid_at_stated_T(gpu, name, dims, steps):
     g = oracle.random_grid(dims, seed=1).astype(np.float32)
     ref, got, _ = run_both(name, g, steps)
     assert np.array_equal(ref.view(np.uint32), got.view(np.uint32))
+
+
+@pytest.mark.parametrize("dims,n", [((130, 300), 4), ((64, 64), 2), ((257, 517), 3)])
+def test_run_batch_grouped_identical_grids(gpu, dims, n):
+    """Identical 2D grids in a batch run as ONE launch per step for the whole group
+    (kModeGroup: per-grid tensor maps in global memory): bitwise each grid's own run,
+    from mixed source buffers, and the same as the interleaved schedule (SST_GROUP=0)."""
+    import torch
+
+    from paper_2506_22969_b200 import run_batch
+
+    engs = []
+    try:
+        grids = [torch.from_numpy(oracle.random_grid(dims, seed=40 + i).astype(np.float32)).cuda() for i in range(n)]
+        for _ in range(n):
+            e = SparseStencil("Box-2D9P", list(dims))
+            e.bind()
+            engs.append(e)
+        srcs = [i & 1 for i in range(n)]
+        for steps in (2, 5):
+            want = []
+            for e, g in zip(engs, grids):
+                e.upload(g, 0)
+                want.append(e.download(e.run(steps, 0)))
+            for mode in ("1", "0"):
+                os.environ["SST_GROUP"] = mode
+                for e, g, s in zip(engs, grids, srcs):
+                    e.upload(g, s)
+                l0 = [e.stats()["launches"] for e in engs]
+                dst = run_batch(engs, steps, srcs)
+                for e, d, w, l in zip(engs, dst, want, l0):
+                    assert np.array_equal(e.download(d).view(np.uint32), w.view(np.uint32)), mode
+                    assert e.stats()["launches"] - l == steps
+    finally:
+        os.environ.pop("SST_GROUP", None)
+        for e in engs:
+            e.close()
