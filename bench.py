@@ -349,7 +349,8 @@ def run_engine(args, cfg, cfg_name):
     torch.cuda.synchronize(dev)
     if ws > 1:
         dist.barrier()
-    _hold_device(stream)
+    if not args.share_gpu:  # (ranks sharing one GPU would spin while the other rank is timed)
+        _hold_device(stream)
     ev0.record(stream)
     if small:
         _step_copies(engines, args.steps // args.fuse, args.fuse, stream.cuda_stream, batch=ws == 1)
