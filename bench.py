@@ -528,8 +528,10 @@ def _hold_device(stream):
     device work, not the host's enqueue latency (the e2e number keeps the host side)."""
     import torch
 
-    with torch.cuda.stream(stream):
-        torch.cuda._sleep(2_000_000)
+    sleep = getattr(torch.cuda, "_sleep", None)  # (torch's spin kernel; absent: no hold)
+    if sleep is not None:
+        with torch.cuda.stream(stream):
+            sleep(2_000_000)
 
 
 def _step_copies(engines, launches, fuse, stream, batch=True):
