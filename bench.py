@@ -554,12 +554,12 @@ def _step_copies(engines, launches, fuse, stream, batch=True):
         engines[i % n].step(fuse)
 
 
-def _sweep_configs(args, skip, device, budget_steps=60):
+def _sweep_configs(args, skip, device, budget_steps=None):
     """Every other BASELINE config on this GPU in the same run (device-resident GStencil/s
     at the config's operator, same timing rules as the headline: CUDA events on the
     launch stream, grids whose ping-pong pair fits in L2 stepped round-robin over
-    independent copies). Steps per config: min(config T, budget_steps), one run of
-    binary16 inter-step storage for the large grids, as the headline."""
+    independent copies). Steps per config: the config's stated T (one run, binary16
+    between steps, as the headline)."""
     import torch
 
     from paper_2506_22969_b200 import estimate_device
@@ -571,7 +571,7 @@ def _sweep_configs(args, skip, device, budget_steps=60):
     for name, (stencil, dims, T) in CONFIGS.items():
         if name == skip:
             continue
-        steps = min(T, budget_steps)
+        steps = T if budget_steps is None else min(T, budget_steps)
         pair = 2 * int(np.prod(dims)) * 4
         small = pair <= 192 << 20
         nrep = (-(-(400 << 20) // pair) + 1) if small else 1
