@@ -10,7 +10,8 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libsparstencil.so"
+LIB_PATH = Path(__file__).resolve().parent / (
+    "libsparstencil_ablation.so" if os.environ.get("SST_LIB") == "ablation" else "libsparstencil.so")
 
 SST_OK = 0
 SST_PREC_F16 = 1

@@ -29,6 +29,14 @@ INCLUDES = [f"-I{REPO / 'include'}", f"-I{CSRC / 'host'}", f"-I{CSRC / 'device'}
 CXXFLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wextra", "-fvisibility=hidden"]
 NVFLAGS = ["-std=c++20", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-fvisibility=hidden",
            "--expt-relaxed-constexpr"]
+# SST_ABLATION=1: compile the kernels' ablation bits in (tools/ablate.py, profiling only;
+# objects go to build_ablation/ and the library to libsparstencil_ablation.so, which
+# SST_LIB=ablation selects at load time)
+ABLATION = os.environ.get("SST_ABLATION") == "1"
+if ABLATION:
+    NVFLAGS += ["-DSST_ABLATION=1"]
+    OBJ = PKG / "build_ablation"
+    LIB = PKG / "libsparstencil_ablation.so"
 
 HOST_SRCS = sorted((CSRC / "host").glob("*.cpp"))
 DEVICE_SRCS = sorted((CSRC / "device").glob("*.cu"))
@@ -71,6 +79,8 @@ def build(verbose: bool = False, force: bool = False) -> Path:
             f.result()
     if force or _stale(LIB, objs):
         _run([NVCC, "-shared", *ARCH, "-cudart", "static", "-o", LIB, *objs], verbose)
+    if ABLATION:  # (the CLI is built from the production objects only)
+        return LIB
     # the CLI (reference tools/main.cpp) links the same objects statically
     cli_src = CSRC / "cli" / "sstensor.cpp"
     cli_obj = OBJ / "sstensor.o"

@@ -187,12 +187,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         Y0 = by * (TYB * kTileH);
     };
 
-    if (warp == 0 && !(p.debug_mode & 32)) {
+    if (warp == 0 && !(dbg(p) & 32)) {
         // ------------------------------------------------------ TMA producer
         if (elect_one()) {
             const uint32_t pbytes = static_cast<uint32_t>(p.patch_w * p.patch_h * ELEM);
             const int ox = p.gx - 2 * p.r, oxc = ox & ~(RW - 1);
-            const bool edge = oxc != ox && bx * (kTXB * kTileW) + kTXB * kTileW > ox && !(p.debug_mode & 24);
+            const bool edge = oxc != ox && bx * (kTXB * kTileW) + kTXB * kTileW > ox && !(dbg(p) & 24);
             int it = 0;
             for_each_run(u0, u1, ozw, p.nby, p.zchunk, [&](int col, int zo_a, int zo_b) {
                 int X0, Y0;
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // input (storage) planes of outputs zo_a..zo_b: zo_a .. zo_b + 2R
                 for (int z = p.slow_lo + zo_a; z <= p.slow_lo + zo_b + 2 * R; ++z, ++it) {
                     const int s = it % NP;
-                    if (p.debug_mode & 16) {  // TMA-only: the producer recycles its own ring
+                    if (dbg(p) & 16) {  // TMA-only: the producer recycles its own ring
                         if (it >= NP) mbar_wait(&patch_full[s], ((it / NP) - 1) & 1);
                     } else {
                         mbar_wait(&patch_empty[s], ((it / NP) & 1) ^ 1);
@@ -215,12 +215,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             });
-            if (p.debug_mode & 16)
+            if (dbg(p) & 16)
                 for (int j = (it > NP ? it - NP : 0); j < it; ++j) mbar_wait(&patch_full[j % NP], (j / NP) & 1);
         }
-    } else if (p.debug_mode & 16) {
+    } else if (dbg(p) & 16) {
         // TMA-only ablation: the other roles idle
-    } else if ((p.debug_mode & 32) && warp < kEpiWarp0) {
+    } else if ((dbg(p) & 32) && warp < kEpiWarp0) {
         // store-only ablation: only the epilogue runs (writes zeros)
     } else if (warp == 1) {
         // -------------------------------------------------------- MMA issuer
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     // K step outer, z slice inner: consecutive MMAs go to the KZ different
                     // accumulators (independent), not KZ chains of dependent ones
-                    const int nk = (p.debug_mode & 4) ? 1 : ksz;
+                    const int nk = (dbg(p) & 4) ? 1 : ksz;
                     for (int ks = 0; ks < nk; ++ks) {
                         const uint64_t bd = make_smem_desc(b0 + ks * 512u, 128, b_sbo);
 #pragma unroll
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int32_t toff[GPW][8];
         tile_offsets<TYB, GPW, ELEM>(gw, p.patch_w, toff);
         const uint32_t gstride = static_cast<uint32_t>(p.k_pad) * 16u;
-        const int nsweeps = (active && !(p.debug_mode & 2)) ? ksz : 0;
+        const int nsweeps = (active && !(dbg(p) & 2)) ? ksz : 0;
         int it = 0;
         for_each_run(u0, u1, ozw, p.nby, p.zchunk, [&](int col, int zo_a, int zo_b) {
             (void)col;
@@ -304,14 +304,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int etid = threadIdx.x - kEpiWarp0 * 32;
         int o = 0, it_base = 0;  // it_base: gather iteration of the run's first input plane
         const int ox = p.gx - 2 * p.r;
-        const bool edge = (ox & (RW - 1)) != 0 && bx * (kTXB * kTileW) + kTXB * kTileW > ox && !(p.debug_mode & 24);
+        const bool edge = (ox & (RW - 1)) != 0 && bx * (kTXB * kTileW) + kTXB * kTileW > ox && !(dbg(p) & 24);
         for_each_run(u0, u1, ozw, p.nby, p.zchunk, [&](int col, int zo_a, int zo_b) {
             int X0, Y0;
             col_xy(col, X0, Y0);
             for (int zo = zo_a; zo <= zo_b; ++zo, ++o) {
                 const int slot = o % NACC;
                 uint32_t v[NBOX][CW];
-                if (p.debug_mode & 32) {
+                if (dbg(p) & 32) {
 #pragma unroll
                     for (int c = 0; c < NBOX; ++c)
 #pragma unroll
@@ -325,19 +325,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (lane == 0) mbar_arrive(&d_empty[slot]);
                 }
                 const uint8_t* ring = nullptr;
-                if (edge && !(p.debug_mode & 32)) {  // center input plane of output zo
+                if (edge && !(dbg(p) & 32)) {  // center input plane of output zo
                     const int ci = it_base + (zo - zo_a) + R;
                     mbar_wait(&ring_full[ci % kRingSlots], (ci / kRingSlots) & 1);
                     ring = sRing + (ci % kRingSlots) * (TYB * kTileH * 16);
                 }
                 if constexpr (HOUT) {
-                    if (!(p.debug_mode & 1))
+                    if (!(dbg(p) & 1))
                         store_batch_h<3, TYB, NS, kEdgeRing, PEER>(
                             p, tmap_out, reinterpret_cast<__half*>(buf_of(p, p.src ^ 1)), v, sS, L.s_stride, o, X0,
                             Y0, p.slow_lo + zo, q, lane, etid, reinterpret_cast<const __half*>(ring),
                             (PEER && (p.peer_mask & 1)) ? &p.peer_maps->up[p.src ^ 1] : nullptr,
                             (PEER && (p.peer_mask & 2)) ? &p.peer_maps->down[p.src ^ 1] : nullptr);
-                } else if (!(p.debug_mode & 1))
+                } else if (!(dbg(p) & 1))
                     store_batch<3, TYB, NS, kEdgeRing, PEER>(
                         p, tmap_out, buf_of(p, p.src ^ 1), v, sS, L.s_stride, o, X0, Y0, p.slow_lo + zo, q, lane,
                         etid, reinterpret_cast<const float*>(ring), (p.peer_mask & 1) ? &p.peer_maps->up[p.src ^ 1] : nullptr,
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         unsigned long long* t = p.trace + 4 * blockIdx.x;
         t[0] = smid();
         t[1] = t_start;
-        t[2] = (p.debug_mode & 1024) ? t_mid : t_main;  // profiling: prologue split
+        t[2] = (dbg(p) & 1024) ? t_mid : t_main;  // profiling: prologue split
         t[3] = global_ns();
     }
     if (warp == 1) {

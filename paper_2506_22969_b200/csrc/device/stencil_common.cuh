@@ -97,6 +97,13 @@ struct StepParams {
     int32_t group_n;
 };
 
+// Ablation bits (tools/ablate.py) are compiled in only with SST_ABLATION=1 (build
+// env): a branch in the epilogue costs store throughput even when never taken.
+#ifndef SST_ABLATION
+#define SST_ABLATION 0
+#endif
+__device__ __forceinline__ int dbg(const StepParams& p) { return SST_ABLATION ? p.debug_mode : 0; }
+
 __device__ __forceinline__ float* buf_of(const StepParams& p, int i) {
     return (i & 1) ? p.buf[1] : p.buf[0];  // select, not a dynamic param-space index
 }
@@ -345,7 +352,7 @@ __device__ __forceinline__ void store_right_edge(const StepParams& p, float* dst
                                                  int Z0, uint32_t q, uint32_t lane) {
     constexpr int NBOX = kTXB / 2;
     const int ox = p.gx - 2 * p.r, ox4 = ox & ~3;
-    if (X0 + kTXB * kTileW <= ox4 || (p.debug_mode & 8)) return;
+    if (X0 + kTXB * kTileW <= ox4 || (dbg(p) & 8)) return;
     const int dxl = static_cast<int>(q) * 4 + static_cast<int>(lane / 8);
     const int y_lim = DIMS == 2 ? p.slow_hi : p.y_end;
     const int y0 = Y0 + static_cast<int>(lane % 8);
@@ -460,7 +467,7 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
     const uint32_t stage = smem_u32(sS) + buf;
     if (etid == 0) bulk_wait_read<NS - 1>();  // this buffer's previous stores have read it
     named_bar_sync(kEpiBarrier, kEpiWarps * 32);
-    if (!(p.debug_mode & 128)) {  // (ablation 128: TMA stores without staging)
+    if (!(dbg(p) & 128)) {  // (ablation 128: TMA stores without staging)
 #pragma unroll
     for (int c = 0; c < NBOX; ++c)
 #pragma unroll
@@ -482,7 +489,7 @@ __device__ __forceinline__ void store_batch(const StepParams& p, const CUtensorM
     if constexpr (DIMS == 2 && PEER)
         if (p.peer_mask != 0 && etid >= 32 && etid < 64 && (Y0 < p.r || Y0 + TYB * kTileH > p.peer_down0))
             peer_right_edge(p, stage, s_stride, X0, Y0, TYB * kTileH, peer_up_buf, peer_down_buf, lane);
-    if (etid == 0 && !(p.debug_mode & 64)) {  // (ablation 64: staging only, no TMA stores)
+    if (etid == 0 && !(dbg(p) & 64)) {  // (ablation 64: staging only, no TMA stores)
         fence_proxy_async_smem();
 #pragma unroll
         for (int c = 0; c < NBOX; ++c) {
@@ -536,7 +543,7 @@ __device__ __forceinline__ void store_right_edge_h(const StepParams& p, __half* 
                                                    int Z0, uint32_t q, uint32_t lane) {
     constexpr int NBOX = kTXB / 2;
     const int ox = p.gx - 2 * p.r, ox8 = ox & ~7;
-    if (X0 + kTXB * kTileW <= ox8 || (p.debug_mode & 8)) return;
+    if (X0 + kTXB * kTileW <= ox8 || (dbg(p) & 8)) return;
     const int dxl = static_cast<int>(q) * 4 + static_cast<int>(lane / 8);
     const int y_lim = DIMS == 2 ? p.slow_hi : p.y_end;
     const int y0 = Y0 + static_cast<int>(lane % 8);
@@ -648,7 +655,7 @@ __device__ __forceinline__ void store_batch_h(const StepParams& p, const CUtenso
     if constexpr (DIMS == 2 && PEER)
         if (p.peer_mask != 0 && etid >= 32 && etid < 64 && (Y0 < p.r || Y0 + TYB * kTileH > p.peer_down0))
             peer_right_edge_h(p, stage, s_stride, X0, Y0, TYB * kTileH, peer_up_buf, peer_down_buf, lane);
-    if (etid == 0 && !(p.debug_mode & 64)) {
+    if (etid == 0 && !(dbg(p) & 64)) {
         fence_proxy_async_smem();
 #pragma unroll
         for (int cb = 0; cb < NBOX / 2; ++cb) {

@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
         return sBid[r % kBidSlots];
     };
 
-    if ((p.debug_mode & 32) && warp < kEpiWarp0) {
+    if ((dbg(p) & 32) && warp < kEpiWarp0) {
         // store-only ablation: only the epilogue runs (writes zeros)
     } else if (warp == 0) {
         // ------------------------------------------------------ TMA producer
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
             tc_fence_after();
             if (elect_one()) {
                 const uint32_t b0 = smem_u32(sB + s * L.b_stride);
-                const int nks = (p.debug_mode & 4) ? 1 : p.nks;
+                const int nks = (dbg(p) & 4) ? 1 : p.nks;
                 for (int ks = 0; ks < nks; ++ks) {
                     const uint64_t bd = make_smem_desc(b0 + ks * 512u, 128, b_sbo);
                     const uint32_t ea = tmem + e_col + static_cast<uint32_t>(ks);
@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
         int32_t toff[GPW][8];
         tile_offsets<TYB, GPW, ELEM>(gw, p.patch_w, toff);
         const uint32_t gstride = static_cast<uint32_t>(p.k_pad) * 16u;  // bytes per 8-tile group
-        const int nsweeps = (active && !(p.debug_mode & 2)) ? p.k_pad / 32 : 0;
+        const int nsweeps = (active && !(dbg(p) & 2)) ? p.k_pad / 32 : 0;
         int r = 0;
         for (int j = 0; dyn || j < total; ++j, ++r) {
             int t, b;
@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
             const uint32_t ph = (r / NACC) & 1;
             ++r;
             uint32_t v[NBOX][CW];
-            if (p.debug_mode & 32) {  // store-only ablation
+            if (dbg(p) & 32) {  // store-only ablation
 #pragma unroll
                 for (int c = 0; c < NBOX; ++c)
 #pragma unroll
@@ -552,23 +552,23 @@ __global__ void __launch_bounds__(kThreads, CPS)
                 if (p.fold_ring != nullptr) fold_keep_ring<TYB>(p, v, X0, Y0, q, lane);
             if constexpr (grp) {  // grouped launch: the grid's map and buffer (global memory)
                 if constexpr (HOUT) {
-                    if (!(p.debug_mode & 1))
+                    if (!(dbg(p) & 1))
                         store_batch_h<DIMS, TYB, NS>(p, &p.group[gj].out, reinterpret_cast<__half*>(p.group[gj].out_buf),
                                                      v, sS, L.s_stride, r - 1, X0, Y0, Z0, q, lane, etid);
-                } else if (!(p.debug_mode & 1)) {
+                } else if (!(dbg(p) & 1)) {
                     store_batch<DIMS, TYB, NS, kEdgePlain, false>(p, &p.group[gj].out, p.group[gj].out_buf, v, sS,
                                                                    L.s_stride, r - 1, X0, Y0, Z0, q, lane, etid);
                 }
             } else if constexpr (HOUT) {
                 const int par = (p.src + t + 1) & 1;
-                if (!(p.debug_mode & 1))
+                if (!(dbg(p) & 1))
                     store_batch_h<DIMS, TYB, NS, kEdgePlain, MODE == kModePeer>(
                         p, &maps.out[par], reinterpret_cast<__half*>(buf_of(p, par)), v, sS, L.s_stride, r - 1, X0,
                         Y0, Z0, q, lane, etid, nullptr, (p.peer_mask & 1) ? &p.peer_maps->up[par] : nullptr,
                         (p.peer_mask & 2) ? &p.peer_maps->down[par] : nullptr,
                         reinterpret_cast<__half*>(par ? p.peer_up_buf[1] : p.peer_up_buf[0]),
                         reinterpret_cast<__half*>(par ? p.peer_down_buf[1] : p.peer_down_buf[0]));
-            } else if (!(p.debug_mode & 1))
+            } else if (!(dbg(p) & 1))
             {
                 const int par = (p.src + t + 1) & 1;
                 store_batch<DIMS, TYB, NS, kEdgePlain, peer>(

@@ -1,10 +1,16 @@
-"""Kernel ablation timing (profiling aid, not a bench): for each config, variant and
+"""Kernel ablation timing (profiling aid, not a bench; needs the profiling build:
+`SST_ABLATION=1 python -m paper_2506_22969_b200.build`): for each config, variant and
 debug mode (1 no stores, 2 no gather, 4 no MMA), time `steps` launches with CUDA
 events and print microseconds per launch. Usage:
     python tools/ablate.py Box-3D27P 512x512x512 [variants=-1,5,6] [modes=0,1,2,4,7] [steps=50]
 """
 import os
 import sys
+
+# the ablation bits are compiled only into the profiling build of the library
+# (SST_ABLATION=1 python -m paper_2506_22969_b200.build -> libsparstencil_ablation.so);
+# modes other than 0 need it, mode 0 alone also runs on the production library
+os.environ.setdefault("SST_LIB", "ablation")
 
 import torch
 
