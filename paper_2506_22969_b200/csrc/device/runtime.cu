@@ -711,6 +711,10 @@ struct sst_plan {
     void h16_step(int src, uint64_t t, uint64_t nsteps, cudaStream_t st) {
         sst::MapSet m;
         sst::StepParams p = h16_params(src, t, nsteps, m);
+        // odd launches of a run draw batches in reverse order: they start on the rows the
+        // previous launch stored last (still in L2); SST_REVERSE=0 off
+        const char* rv = std::getenv("SST_REVERSE");
+        p.reverse = (rv && std::atoi(rv) == 0) ? 0 : static_cast<int32_t>(t & 1);
         h16_issue(p, m, t > 0, t + 1 < nsteps, p.nbatch, st);
     }
 

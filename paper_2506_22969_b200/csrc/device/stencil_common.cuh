@@ -95,6 +95,7 @@ struct StepParams {
     int32_t fold_w;            // 1D fold: interior cells per view row
     const GroupMaps* group;    // grouped launch (kModeGroup): per grid maps, group_n grids of nbatch batches
     int32_t group_n;
+    int32_t reverse;           // dynamic single-step launches: batches drawn in reverse order
 };
 
 // Ablation bits (tools/ablate.py) are compiled in only with SST_ABLATION=1 (build

@@ -255,6 +255,8 @@ __global__ void __launch_bounds__(kThreads, CPS)
         b = static_cast<int>(blockIdx.x) + (j - t * nper) * G;
     };
     auto batch_coords = [&](int b, int& X0, int& Y0, int& Z0) {
+        if constexpr (MODE == kModeDynamic)  // reverse traversal: start where the previous step ended
+            if (p.reverse) b = p.nbatch - 1 - b;
         X0 = (b % nbx) * (kTXB * kTileW);
         Y0 = ((b / nbx) % nby) * (TYB * kTileH) + (DIMS == 2 ? p.slow_lo : 0);
         Z0 = b / (nbx * nby) + (DIMS == 3 ? p.slow_lo : 0);
