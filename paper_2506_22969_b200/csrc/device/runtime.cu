@@ -759,6 +759,8 @@ struct sst_plan {
             const int kind = t == 0 ? 0 : t + 1 == L ? 3 : 1 + static_cast<int>(t & 1);
             p.group = d_group + static_cast<std::size_t>(kind) * G;
             p.group_n = static_cast<int32_t>(G);
+            const char* rv = std::getenv("SST_REVERSE");  // (as h16_step: odd launches in reverse)
+            p.reverse = (rv && std::atoi(rv) == 0) ? 0 : static_cast<int32_t>(t & 1);
             h16_issue(p, m, t > 0, t + 1 < L, p.nbatch * static_cast<int>(G), st);
         }
     }

@@ -300,24 +300,27 @@ __global__ void __launch_bounds__(kThreads, CPS)
             if (lane == 0) q1 = static_cast<uint32_t>(G) + atomicAdd(p.sched, 1u) - p.sched_base;
             // one draw covers kDrawGroup consecutive batches (fewer same-address atomics)
             auto item = [&](uint32_t& slot) -> bool {
-                uint32_t grp = 0;
+                uint32_t dgrp = 0;  // draw group (kDrawGroup consecutive items)
                 if (lane == 0) {
-                    grp = slot;
-                    if (grp * static_cast<uint32_t>(kDrawGroup) < static_cast<uint32_t>(nitems))
+                    dgrp = slot;
+                    if (dgrp * static_cast<uint32_t>(kDrawGroup) < static_cast<uint32_t>(nitems))
                         slot = static_cast<uint32_t>(G) + atomicAdd(p.sched, 1u) - p.sched_base;
                 }
                 for (int e = 0; e < kDrawGroup; ++e) {
                 int g = -1;
                 if (lane == 0) {
-                    const uint32_t gi = grp * static_cast<uint32_t>(kDrawGroup) + static_cast<uint32_t>(e);
+                    const uint32_t gi = dgrp * static_cast<uint32_t>(kDrawGroup) + static_cast<uint32_t>(e);
                     g = gi < static_cast<uint32_t>(nitems) ? static_cast<int>(gi) : -1;
                     sBid[r % kBidSlots] = g;
                     mbar_arrive(&bid_full[r % kBidSlots]);
                 }
                 g = __shfl_sync(0xffffffffu, g, 0);
                 if (g < 0) return false;
-                const int t = mdyn ? g / p.nbatch : 0, gj = grp ? g / p.nbatch : 0;
-                const int b = mdyn ? g - t * p.nbatch : grp ? g - gj * p.nbatch : g;
+                if constexpr (MODE == kModeGroup)  // reverse traversal of the whole group
+                    if (p.reverse) g = nitems - 1 - g;
+                constexpr bool group_mode = MODE == kModeGroup;
+                const int t = mdyn ? g / p.nbatch : 0, gj = group_mode ? g / p.nbatch : 0;
+                const int b = mdyn ? g - t * p.nbatch : group_mode ? g - gj * p.nbatch : g;
                 int X0, Y0, Z0;
                 batch_coords(b, X0, Y0, Z0);
                 if constexpr (mdyn) {
@@ -509,6 +512,7 @@ __global__ void __launch_bounds__(kThreads, CPS)
                     b -= t * p.nbatch;
                 }
                 if constexpr (grp) {
+                    if (p.reverse) b = nitems - 1 - b;
                     gj = b / p.nbatch;
                     b -= gj * p.nbatch;
                 }
